@@ -1,0 +1,140 @@
+/*
+ * spmvlab_cuda.h -- C ABI of the B200-native (sm_100a) SpMV hot path.
+ *
+ * This is the drop-in boundary for the reference library's algorithm interface
+ * (/root/reference/proj/include/spmvlab/engine.hpp).  Each entry point names the reference
+ * function it replaces.  Plain pointers and sizes only; all matrix / vector pointers are DEVICE
+ * pointers unless the name says _host.  `stream` is a cudaStream_t passed as void* (NULL = the
+ * legacy default stream).  Calls are stream-ordered; the C++ wrapper in
+ * include/spmvlab_cuda/engine.hpp synchronises to give the reference's synchronous semantics.
+ *
+ * Return codes: 0 = ok; 1 + spmvlab::ErrorKind ordinal (inc/types.hpp:47-62), i.e.
+ *   1 DimensionMismatch, 2 InvalidArgument, 3 CorruptFormat, 4 Overflow, 9 IndexOutOfRange,
+ *   10 DuplicateEntry; >= 100 CUDA / allocation faults.  spmvlab_cuda_last_error() describes the
+ *   last failure on the calling thread.
+ *
+ * Algorithm ordinals follow inc/engine.hpp:30-42:
+ *   0 crs, 1 parcrs, 2 merge, 3 csb, 4 csbh, 5 bcoh, 6 bcohc, 7 bcohch, 8 bcohchp, 9 mergeb,
+ *   10 mergebh.
+ */
+#ifndef SPMVLAB_CUDA_H
+#define SPMVLAB_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMVLAB_CUDA_ABI_VERSION 1
+
+/* Opaque, device-resident, immutable format (a BuiltFormat, inc/engine.hpp:82). */
+typedef struct spmvlab_cuda_format spmvlab_cuda_format;
+
+/* TripletMatrix view (inc/triplet.hpp:30-38), device pointers, u32 indices, f64 values. */
+typedef struct {
+  uint32_t m;
+  uint32_t n;
+  uint64_t nnz;
+  const uint32_t* row_ind;
+  const uint32_t* col_ind;
+  const double* data;
+} spmvlab_cuda_coo;
+
+/* EngineOptions (inc/engine.hpp:75-79). */
+typedef struct {
+  uint64_t l2_bytes;        /* default 512 KiB (inc/block_size.hpp:39) */
+  uint64_t split_threshold; /* 0 = 2*beta (inc/spmv_parallel.hpp:205-207) */
+  uint32_t build_threads;   /* accepted for interface parity; the GPU build ignores it */
+} spmvlab_cuda_options;
+
+/* StorageArray (inc/storage.hpp:32-36). */
+typedef struct {
+  char name[32];
+  uint64_t bytes;
+} spmvlab_cuda_storage_array;
+
+typedef struct {
+  int alg;
+  uint32_t m, n;
+  uint64_t nnz;
+  uint32_t log2_beta, block_rows, block_cols;
+  uint32_t element_level, block_level, bands;
+  uint32_t merge_tiles, work_items;
+} spmvlab_cuda_format_info;
+
+int spmvlab_cuda_abi_version(void);
+const char* spmvlab_cuda_last_error(void);
+
+/* build_format(Algorithm, const TripletMatrix&, threads, EngineOptions)  -- inc/engine.hpp:96-122.
+ * `threads` is the BCOH band count p (inc/engine.hpp:108-115), ignored by the other formats. */
+int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threads,
+                              const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
+                              void* stream);
+
+/* run_spmv(Algorithm, const BuiltFormat&, const DenseVector& x, DenseVector& y, p, opt)
+ * -- inc/engine.hpp:126-148.  y (length m) is fully overwritten.  p must be >= 1 and, for BCOH,
+ * equal to the band count (inc/spmv_parallel.hpp:339-341). */
+int spmvlab_cuda_run_spmv(int alg, const spmvlab_cuda_format* f, const double* x, uint64_t x_len,
+                          double* y, uint64_t y_len, unsigned p, const spmvlab_cuda_options* opt,
+                          void* stream);
+
+/* Same multiply with HOST x / y (pinned or pageable): H2D x, multiply, D2H y on `stream`, using
+ * caller-provided device staging buffers x_dev (n doubles) and y_dev (m doubles). */
+int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const double* x_host,
+                               uint64_t x_len, double* y_host, uint64_t y_len, unsigned p,
+                               const spmvlab_cuda_options* opt, double* x_dev, double* y_dev,
+                               void* stream);
+
+/* storage_report(const BuiltFormat&) -- inc/engine.hpp:158-160 / inc/storage.hpp:62-123. */
+int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,
+                                size_t capacity, size_t* count);
+
+int spmvlab_cuda_get_format_info(const spmvlab_cuda_format* f, spmvlab_cuda_format_info* info);
+
+/* Device pointer + byte count of one named array (storage arrays use the reference's names;
+ * BCOH also exposes band_* and off_* tables).  For parity downloads. */
+int spmvlab_cuda_format_array(const spmvlab_cuda_format* f, const char* name, const void** dev_ptr,
+                              uint64_t* bytes);
+
+/* Synchronous copy of one named array into host memory (capacity in bytes; *bytes = its size). */
+int spmvlab_cuda_download_array(const spmvlab_cuda_format* f, const char* name, void* host_dst,
+                                uint64_t capacity, uint64_t* bytes);
+
+void spmvlab_cuda_free_format(spmvlab_cuda_format* f);
+
+/* validate(const TripletMatrix&) -- inc/triplet.hpp:42-59 (range + duplicate check on device). */
+int spmvlab_cuda_validate(const spmvlab_cuda_coo* a, void* stream);
+
+/* --- primitives, exposed for parity tests ---------------------------------------------------- */
+
+/* select_block_size -- inc/block_size.hpp:47-61 (value_size 8). Host computation. */
+unsigned spmvlab_cuda_select_block_size(uint64_t n, unsigned index_bits_cap, uint64_t l2_bytes);
+
+/* partition_rows_by_nnz -- inc/block_size.hpp:73-102.  Host arrays. */
+int spmvlab_cuda_partition_rows_by_nnz(const uint32_t* prefix_host, uint32_t m, unsigned p,
+                                       unsigned log2_beta, uint32_t* bounds_host);
+
+/* diagonal_search over A = a[0..a_len) and B = b[0..b_len) (b == NULL: B[j] = j, the CRS case)
+ * (inc/spmv_parallel.hpp:47-69), for `count` diagonals at once on the device:
+ * out_i[k] = i of diags[k] (j = diag - i). */
+int spmvlab_cuda_merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b,
+                                   uint64_t b_len, const uint64_t* diags, uint64_t count,
+                                   uint64_t* out_i, void* stream);
+
+/* Curve keys on device: kind 0 = Z-Morton, 1 = Hilbert (inc/curves.hpp:107-143). */
+int spmvlab_cuda_curve_keys(int kind, const uint32_t* rows, const uint32_t* cols, uint64_t count,
+                            unsigned level, uint64_t* keys, void* stream);
+
+/* Radix sort of (key, value) pairs by key bits [begin_bit, end_bit), in place, stable. */
+int spmvlab_cuda_sort_pairs(uint64_t* keys, uint32_t* values, uint64_t count, int begin_bit,
+                            int end_bit, void* stream);
+
+/* Exclusive scan: out[0..n] (out[n] = total). */
+int spmvlab_cuda_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMVLAB_CUDA_H */

@@ -1,0 +1,227 @@
+// ref_shim.cpp -- C-ABI shim over the UNMODIFIED reference headers (TEST INFRASTRUCTURE ONLY).
+//
+// Compiled by oracle/Makefile directly against /root/reference/proj/include (nothing is copied)
+// into oracle/_ref/libspmvref.so.  It lets the tests pin the C restatement (spmv_oracle.c)
+// against the reference itself, lets tests/golden/make_golden.py record golden vectors, and is
+// bench.py --impl reference's CPU arm (the reference's own engines, multithreaded).
+//
+// Formats are exported with the same named-array layout as orc_format (spmv_oracle.h): the
+// storage_report arrays first (inc/storage.hpp:62-123), BCOH bands concatenated with off_* tables.
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "spmv_oracle.h"
+#include "spmvlab/bench.hpp"
+#include "spmvlab/engine.hpp"
+
+using namespace spmvlab;
+
+namespace {
+
+thread_local std::string g_err;
+
+int code_of(const Error& e) { return static_cast<int>(e.kind()) + 1; }
+
+template <typename T>
+void put(orc_format* f, const char* name, const std::vector<T>& v) {
+  orc_array* a = &f->arrays[f->narrays++];
+  std::strncpy(a->name, name, sizeof(a->name) - 1);
+  a->elem_size = sizeof(T);
+  a->bytes = v.size() * sizeof(T);
+  a->data = std::malloc(a->bytes ? a->bytes : 1);
+  if (a->bytes) std::memcpy(a->data, v.data(), a->bytes);
+}
+
+struct Handle {
+  Algorithm alg;
+  BuiltFormat fmt;
+};
+
+TripletMatrix make_triplet(uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows,
+                           const uint32_t* cols, const double* vals) {
+  TripletMatrix a;
+  a.m = m;
+  a.n = n;
+  a.row_ind.assign(rows, rows + nnz);
+  a.col_ind.assign(cols, cols + nnz);
+  a.data.assign(vals, vals + nnz);
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_build(int alg, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows,
+              const uint32_t* cols, const double* vals, unsigned threads, uint64_t l2_bytes,
+              unsigned build_threads, void** out) {
+  try {
+    auto a = make_triplet(m, n, nnz, rows, cols, vals);
+    EngineOptions opt{l2_bytes, 0, build_threads};
+    auto h = std::make_unique<Handle>(
+        Handle{static_cast<Algorithm>(alg), build_format(static_cast<Algorithm>(alg), a, threads, opt)});
+    *out = h.release();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+void ref_free(void* h) { delete static_cast<Handle*>(h); }
+
+int ref_run(void* hv, int alg, const double* x, uint64_t x_len, double* y, uint64_t y_len,
+            unsigned p, uint64_t split_threshold) {
+  try {
+    auto* h = static_cast<Handle*>(hv);
+    DenseVector xv(x, x + x_len), yv(y_len, 0.0);
+    EngineOptions opt{default_l2_bytes, split_threshold, 1};
+    run_spmv(static_cast<Algorithm>(alg), h->fmt, xv, yv, p, opt);
+    std::memcpy(y, yv.data(), y_len * sizeof(double));
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+// Times `reps` multiplies after `warmup` (min and total seconds), on resident std::vectors, i.e.
+// exactly the reference's min_time_of protocol (inc/bench.hpp:98-110).
+int ref_time_spmv(void* hv, int alg, const double* x, uint64_t x_len, uint64_t y_len, unsigned p,
+                  unsigned reps, unsigned warmup, double* min_s, double* total_s) {
+  try {
+    auto* h = static_cast<Handle*>(hv);
+    DenseVector xv(x, x + x_len), yv(y_len, 0.0);
+    EngineOptions opt{};
+    for (unsigned w = 0; w < warmup; ++w) run_spmv(static_cast<Algorithm>(alg), h->fmt, xv, yv, p, opt);
+    double best = 1e300, tot = 0;
+    for (unsigned r = 0; r < reps; ++r) {
+      auto t0 = std::chrono::steady_clock::now();
+      run_spmv(static_cast<Algorithm>(alg), h->fmt, xv, yv, p, opt);
+      auto t1 = std::chrono::steady_clock::now();
+      const double s = std::chrono::duration<double>(t1 - t0).count();
+      best = s < best ? s : best;
+      tot += s;
+    }
+    *min_s = best;
+    *total_s = tot;
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// Exports the built format as an orc_format (named arrays).
+int ref_export(void* hv, orc_format** out) {
+  auto* h = static_cast<Handle*>(hv);
+  auto* f = static_cast<orc_format*>(std::calloc(1, sizeof(orc_format)));
+  f->alg = static_cast<int>(h->alg);
+  if (auto* c = std::get_if<CrsMatrix>(&h->fmt)) {
+    f->m = c->m; f->n = c->n; f->nnz = c->nnz();
+    put(f, "row_ptr", c->row_ptr); put(f, "col_ind", c->col_ind); put(f, "data", c->data);
+    f->nstorage = 3;
+  } else if (auto* c = std::get_if<CsbMatrix>(&h->fmt)) {
+    f->m = c->m; f->n = c->n; f->nnz = c->nnz();
+    f->log2_beta = c->beta.log2_beta; f->block_rows = c->block_rows; f->block_cols = c->block_cols;
+    put(f, "blk_ptr", c->blk_ptr); put(f, "packed", c->packed); put(f, "data", c->data);
+    f->nstorage = 3;
+  } else if (auto* c = std::get_if<MergeBlockMatrix>(&h->fmt)) {
+    f->m = c->m; f->n = c->n; f->nnz = c->nnz();
+    f->log2_beta = c->beta.log2_beta; f->block_rows = c->block_rows; f->block_cols = c->block_cols;
+    put(f, "blk_row_ptr", c->blk_row_ptr); put(f, "blk_col_ind", c->blk_col_ind);
+    put(f, "blk_data_ptr", c->blk_data_ptr); put(f, "packed", c->packed); put(f, "data", c->data);
+    f->nstorage = 5;
+  } else {
+    const auto& bm = std::get<BcohMatrix>(h->fmt);
+    f->m = bm.m; f->n = bm.n; f->nnz = bm.nnz();
+    f->log2_beta = bm.beta.log2_beta; f->block_rows = bm.block_rows; f->block_cols = bm.block_cols;
+    f->element_level = bm.element_level; f->block_level = bm.block_level;
+    f->bands = static_cast<uint32_t>(bm.bands.size());
+    std::vector<uint32_t> block_nnz, blk_ptr, packed, bfr, brc, bfbr, bbrc;
+    std::vector<int16_t> rjb, cjb;
+    std::vector<uint16_t> col_inc, row_jump;
+    std::vector<double> data;
+    std::vector<uint64_t> oe, ob, orjb, obp, orj;
+    for (const auto& b : bm.bands) {
+      oe.push_back(data.size()); ob.push_back(block_nnz.size()); orjb.push_back(rjb.size());
+      obp.push_back(blk_ptr.size()); orj.push_back(row_jump.size());
+      block_nnz.insert(block_nnz.end(), b.block_nnz.begin(), b.block_nnz.end());
+      rjb.insert(rjb.end(), b.row_jump_block.begin(), b.row_jump_block.end());
+      cjb.insert(cjb.end(), b.col_jump_block.begin(), b.col_jump_block.end());
+      blk_ptr.insert(blk_ptr.end(), b.blk_ptr.begin(), b.blk_ptr.end());
+      col_inc.insert(col_inc.end(), b.col_inc.begin(), b.col_inc.end());
+      row_jump.insert(row_jump.end(), b.row_jump.begin(), b.row_jump.end());
+      packed.insert(packed.end(), b.packed.begin(), b.packed.end());
+      data.insert(data.end(), b.data.begin(), b.data.end());
+      bfr.push_back(b.first_row); brc.push_back(b.row_count);
+      bfbr.push_back(b.first_block_row); bbrc.push_back(b.block_row_count);
+    }
+    oe.push_back(data.size()); ob.push_back(block_nnz.size()); orjb.push_back(rjb.size());
+    obp.push_back(blk_ptr.size()); orj.push_back(row_jump.size());
+    put(f, "block_nnz", block_nnz); put(f, "row_jump_block", rjb); put(f, "col_jump_block", cjb);
+    put(f, "blk_ptr", blk_ptr); put(f, "col_inc", col_inc); put(f, "row_jump", row_jump);
+    put(f, "packed", packed); put(f, "data", data);
+    f->nstorage = 8;
+    put(f, "band_first_row", bfr); put(f, "band_row_count", brc);
+    put(f, "band_first_block_row", bfbr); put(f, "band_block_row_count", bbrc);
+    put(f, "off_elem", oe); put(f, "off_block", ob); put(f, "off_row_jump_block", orjb);
+    put(f, "off_blk_ptr", obp); put(f, "off_row_jump", orj);
+  }
+  // storage_report totals are checked against these arrays by the tests.
+  *out = f;
+  return 0;
+}
+
+void ref_free_export(orc_format* f) {
+  if (!f) return;
+  for (int i = 0; i < f->narrays; ++i) std::free(f->arrays[i].data);
+  std::free(f);
+}
+
+uint64_t ref_storage_total(void* hv) {
+  return storage_report(static_cast<Handle*>(hv)->fmt).total();
+}
+
+// --- primitives (for golden vectors) ---------------------------------------------------------
+unsigned ref_select_block_size(uint64_t n, unsigned cap, uint64_t l2) {
+  return select_block_size(n, cap, l2).log2_beta;
+}
+uint64_t ref_morton(uint32_t r, uint32_t c, unsigned level) { return morton_encode(r, c, level).value; }
+uint64_t ref_hilbert(uint32_t r, uint32_t c, unsigned level) { return hilbert_encode(r, c, level).value; }
+void ref_diagonal_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len,
+                         uint64_t diag, uint64_t* i, uint64_t* j) {
+  auto pt = diagonal_search(std::span<const index_t>(a, a_len), std::span<const index_t>(b, b_len), diag);
+  *i = pt.i;
+  *j = pt.j;
+}
+int ref_partition_rows_by_nnz(const uint32_t* prefix, uint32_t m, unsigned p, unsigned lb,
+                              uint32_t* bounds) {
+  try {
+    auto v = partition_rows_by_nnz(std::span<const index_t>(prefix, m + 1), p, make_block_size(lb));
+    std::memcpy(bounds, v.data(), v.size() * sizeof(uint32_t));
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+void ref_verification_input(uint32_t n, uint64_t seed, double* x) {
+  auto v = verification_input(n, seed);
+  std::memcpy(x, v.data(), n * sizeof(double));
+}
+unsigned ref_hardware_threads() { return hardware_threads(); }
+
+}  // extern "C"

@@ -1,0 +1,11 @@
+"""spmvlab-b200: B200-native (sm_100a) SpMV hot path of arXiv 2502.19284.
+
+The product is libspmvlab_cuda.so (C ABI: include/spmvlab_cuda.h); this package is its Python
+host mirror of the reference's algorithm interface (inc/engine.hpp).
+"""
+from .engine import (  # noqa: F401
+    Algorithm, BuiltFormat, EngineOptions, Error, ErrorKind, StorageBreakdown, TripletMatrix,
+    algorithm_from_name, algorithm_name, all_algorithms, build_format, curve_keys,
+    engine_block_size, exclusive_scan, merge_path_search, partition_rows_by_nnz, run_spmv,
+    run_spmv_host, select_block_size, sort_pairs, storage_report, validate,
+)

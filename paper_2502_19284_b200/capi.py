@@ -1,0 +1,79 @@
+"""ctypes binding of the C ABI declared in include/spmvlab_cuda.h.
+
+The shared library is built in-tree (paper_2502_19284_b200/build.py) for sm_100a.  There is no
+fallback: if the library is missing, importing the product API raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB
+
+_lib = None
+
+# Every symbol include/spmvlab_cuda.h declares (checked by tests/test_capi_cpu.py).
+EXPORTS = [
+    "spmvlab_cuda_abi_version", "spmvlab_cuda_last_error", "spmvlab_cuda_build_format",
+    "spmvlab_cuda_run_spmv", "spmvlab_cuda_run_spmv_host", "spmvlab_cuda_storage_report",
+    "spmvlab_cuda_get_format_info", "spmvlab_cuda_format_array", "spmvlab_cuda_download_array",
+    "spmvlab_cuda_free_format", "spmvlab_cuda_validate", "spmvlab_cuda_select_block_size",
+    "spmvlab_cuda_partition_rows_by_nnz", "spmvlab_cuda_merge_path_search",
+    "spmvlab_cuda_curve_keys", "spmvlab_cuda_sort_pairs", "spmvlab_cuda_exclusive_scan",
+]
+
+
+class Coo(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("n", C.c_uint32), ("nnz", C.c_uint64), ("row_ind", C.c_void_p),
+                ("col_ind", C.c_void_p), ("data", C.c_void_p)]
+
+
+class Options(C.Structure):
+    _fields_ = [("l2_bytes", C.c_uint64), ("split_threshold", C.c_uint64), ("build_threads", C.c_uint32)]
+
+
+class StorageArray(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("bytes", C.c_uint64)]
+
+
+class FormatInfo(C.Structure):
+    _fields_ = [("alg", C.c_int), ("m", C.c_uint32), ("n", C.c_uint32), ("nnz", C.c_uint64),
+                ("log2_beta", C.c_uint32), ("block_rows", C.c_uint32), ("block_cols", C.c_uint32),
+                ("element_level", C.c_uint32), ("block_level", C.c_uint32), ("bands", C.c_uint32),
+                ("merge_tiles", C.c_uint32), ("work_items", C.c_uint32)]
+
+
+def lib_path() -> str:
+    return LIB
+
+
+def load() -> C.CDLL:
+    """Loads libspmvlab_cuda.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        raise RuntimeError(f"CUDA library not built: {LIB} (run __graft_entry__.build())")
+    L = C.CDLL(LIB)
+    vp, u32, u64, i = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+    L.spmvlab_cuda_abi_version.restype = i
+    L.spmvlab_cuda_last_error.restype = C.c_char_p
+    L.spmvlab_cuda_build_format.argtypes = [i, C.POINTER(Coo), C.c_uint, C.POINTER(Options), C.POINTER(vp), vp]
+    L.spmvlab_cuda_run_spmv.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp]
+    L.spmvlab_cuda_run_spmv_host.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp, vp, vp]
+    L.spmvlab_cuda_storage_report.argtypes = [vp, C.POINTER(StorageArray), C.c_size_t, C.POINTER(C.c_size_t)]
+    L.spmvlab_cuda_get_format_info.argtypes = [vp, C.POINTER(FormatInfo)]
+    L.spmvlab_cuda_format_array.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(u64)]
+    L.spmvlab_cuda_download_array.argtypes = [vp, C.c_char_p, vp, u64, C.POINTER(u64)]
+    L.spmvlab_cuda_free_format.argtypes = [vp]
+    L.spmvlab_cuda_free_format.restype = None
+    L.spmvlab_cuda_validate.argtypes = [C.POINTER(Coo), vp]
+    L.spmvlab_cuda_select_block_size.restype = C.c_uint
+    L.spmvlab_cuda_select_block_size.argtypes = [u64, C.c_uint, u64]
+    L.spmvlab_cuda_partition_rows_by_nnz.argtypes = [vp, u32, C.c_uint, C.c_uint, vp]
+    L.spmvlab_cuda_merge_path_search.argtypes = [vp, u64, vp, u64, vp, u64, vp, vp]
+    L.spmvlab_cuda_curve_keys.argtypes = [i, vp, vp, u64, C.c_uint, vp, vp]
+    L.spmvlab_cuda_sort_pairs.argtypes = [vp, vp, u64, i, i, vp]
+    L.spmvlab_cuda_exclusive_scan.argtypes = [vp, vp, u64, vp]
+    _lib = L
+    return L

@@ -1,0 +1,335 @@
+// capi.cu -- the extern "C" boundary (include/spmvlab_cuda.h) over the sm_100a kernels.
+//
+// Mirrors the reference's algorithm interface (inc/engine.hpp:84-160): engine_block_size,
+// build_format, run_spmv (argument checks of check_spmv_args, inc/spmv_parallel.hpp:90-99, and the
+// BCOH band check, :339-341), storage_report.  Errors become return codes (ErrorKind + 1).
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spmvcu {
+thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// select_block_size, inc/block_size.hpp:47-61
+static unsigned select_block_size(uint64_t n, unsigned cap, uint64_t l2_bytes) {
+  if (n < 1) n = 1;
+  const unsigned ceil_log2_n = n <= 1 ? 0 : bit_width64(n - 1);
+  unsigned lb = 3 + (ceil_log2_n + 1) / 2;
+  while (lb > 1) {
+    const uint64_t beta = 1ull << lb;
+    if (lb <= cap && 2 * beta * 8 <= l2_bytes / 2) break;
+    --lb;
+  }
+  return lb;
+}
+
+// engine_block_size, inc/engine.hpp:84-91
+static unsigned engine_log2_beta(int alg, uint32_t n, uint64_t l2_bytes) {
+  return select_block_size(n < 1 ? 1 : n, is_bcoh_alg(alg) ? 15u : 16u, l2_bytes);
+}
+
+// partition_rows_by_nnz, inc/block_size.hpp:73-102 (host; also used by the BCOH build)
+int partition_rows_by_nnz_host(const uint32_t* prefix, uint32_t m, unsigned p, unsigned lb,
+                               uint32_t* bounds) {
+  if (p < 1) return fail(kInvalidArgument, "thread count must be >= 1");
+  const uint64_t nnz = prefix[m];
+  const uint32_t beta = 1u << lb;
+  const uint32_t block_rows = (uint32_t)(((uint64_t)m + beta - 1) >> lb);
+  for (unsigned k = 0; k <= p; ++k) bounds[k] = m;
+  bounds[0] = 0;
+  uint32_t prev_cut = 0;
+  for (unsigned k = 1; k < p; ++k) {
+    const uint64_t target = nnz * k;
+    uint64_t lo = 0, hi = (uint64_t)m + 1;
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if ((uint64_t)prefix[mid] * p < target) lo = mid + 1; else hi = mid;
+    }
+    uint32_t cut = (uint32_t)((lo + beta / 2) >> lb);
+    const uint32_t hic = block_rows >= p ? block_rows - (p - k) : block_rows;
+    const uint32_t loc = prev_cut + 1 < hic ? prev_cut + 1 : hic;
+    if (cut < loc) cut = loc;
+    if (cut > hic) cut = hic;
+    const uint64_t b = (uint64_t)cut << lb;
+    bounds[k] = b < m ? (uint32_t)b : m;
+    prev_cut = cut;
+  }
+  return kOk;
+}
+
+}  // namespace spmvcu
+
+using namespace spmvcu;
+
+// ---------------------------------------------------------------- Format methods
+
+spmvlab_cuda_format::~spmvlab_cuda_format() {
+  for (auto& a : arrays)
+    if (a.ptr) cudaFree(a.ptr);
+}
+
+DevArray* spmvlab_cuda_format::find(const std::string& name) {
+  for (auto& a : arrays)
+    if (a.name == name) return &a;
+  return nullptr;
+}
+const DevArray* spmvlab_cuda_format::find(const std::string& name) const {
+  for (auto& a : arrays)
+    if (a.name == name) return &a;
+  return nullptr;
+}
+
+void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t esz, cudaStream_t) {
+  DevArray a;
+  a.name = name;
+  a.esz = esz;
+  a.bytes = count * esz;
+  // 16-byte padded so vector / bulk loads may over-read the tail safely.
+  const uint64_t alloc = ((a.bytes + 15) & ~uint64_t(15)) + 16;
+  if (cudaMalloc(&a.ptr, alloc) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  arrays.push_back(a);
+  return a.ptr;
+}
+
+void spmvlab_cuda_format::set_count(const std::string& name, uint64_t count) {
+  if (DevArray* a = find(name)) a->bytes = count * a->esz;
+}
+
+// ---------------------------------------------------------------- C ABI
+
+extern "C" {
+
+int spmvlab_cuda_abi_version(void) { return SPMVLAB_CUDA_ABI_VERSION; }
+
+const char* spmvlab_cuda_last_error(void) { return g_last_error.c_str(); }
+
+unsigned spmvlab_cuda_select_block_size(uint64_t n, unsigned cap, uint64_t l2_bytes) {
+  return select_block_size(n, cap, l2_bytes);
+}
+
+int spmvlab_cuda_partition_rows_by_nnz(const uint32_t* prefix, uint32_t m, unsigned p, unsigned lb,
+                                       uint32_t* bounds) {
+  return partition_rows_by_nnz_host(prefix, m, p, lb, bounds);
+}
+
+int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threads,
+                              const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
+                              void* stream) {
+  if (!out || !a) return fail(kInvalidArgument, "null argument");
+  *out = nullptr;
+  if (alg < 0 || alg >= kAlgCount) return fail(kInvalidArgument, "unknown algorithm");
+  if ((uint64_t)a->m > (1ull << 31) || (uint64_t)a->n > (1ull << 31))
+    return fail(kOverflow, "matrix dimension exceeds the supported index width");
+  if (a->nnz > 0xFFFFFFFFull) return fail(kOverflow, "nnz does not fit the 32-bit index type");
+  if (a->nnz && (!a->row_ind || !a->col_ind || !a->data)) return fail(kInvalidArgument, "null COO array");
+  const uint64_t l2 = opt ? opt->l2_bytes : 512 * 1024;
+  const uint64_t split = opt ? opt->split_threshold : 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* f = new (std::nothrow) spmvlab_cuda_format();
+  if (!f) return fail(kNoMemory, "host allocation failed");
+  f->alg = alg;
+  f->m = a->m;
+  f->n = a->n;
+  f->nnz = a->nnz;
+  const unsigned lb = engine_log2_beta(alg, a->n, l2);
+  int rc;
+  {
+    Arena ar(s);
+    if (is_crs_alg(alg)) {
+      rc = build_crs(*f, *a, ar);
+      if (rc == kOk) rc = build_merge_plan(*f, ar);
+    } else if (is_csb_alg(alg)) {
+      rc = build_csb(*f, *a, lb, alg == kCsbh, split, ar);
+    } else if (is_mergeb_alg(alg)) {
+      rc = build_mergeb(*f, *a, lb, alg == kMergeBH, ar);
+    } else {
+      rc = build_bcoh(*f, *a, lb, threads, ar);
+    }
+    ar.release();
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == kOk) rc = check_launch("build_format");
+  }
+  if (rc != kOk) {
+    if (g_last_error.empty() || rc < 100) {
+      switch (rc) {
+        case kIndexOutOfRange: g_last_error = "index out of range: entry outside the matrix shape"; break;
+        case kDuplicateEntry: g_last_error = "duplicate entry: duplicate (row, col) coordinate"; break;
+        case kNoMemory: g_last_error = "device allocation failed"; break;
+        default: break;
+      }
+    }
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return kOk;
+}
+
+int spmvlab_cuda_run_spmv(int alg, const spmvlab_cuda_format* f, const double* x, uint64_t x_len,
+                          double* y, uint64_t y_len, unsigned p, const spmvlab_cuda_options* opt,
+                          void* stream) {
+  if (!f) return fail(kInvalidArgument, "null format");
+  if (x_len != f->n)
+    return fail(kDimensionMismatch, "x has length " + std::to_string(x_len) + ", matrix has " +
+                                        std::to_string(f->n) + " columns");
+  if (y_len != f->m)
+    return fail(kDimensionMismatch, "y has length " + std::to_string(y_len) + ", matrix has " +
+                                        std::to_string(f->m) + " rows");
+  if (alg != kSeqCrs && p < 1) return fail(kInvalidArgument, "worker count must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  (void)opt;
+  switch (alg) {
+    case kSeqCrs:
+    case kParCrs:
+    case kMerge:
+      if (!is_crs_alg(f->alg)) return fail(kInvalidArgument, "format is not CRS");
+      return alg == kSeqCrs ? spmv_seq_crs(*f, x, y, s)
+                            : (alg == kParCrs ? spmv_par_crs(*f, x, y, s) : spmv_merge(*f, x, y, s));
+    case kCsb:
+    case kCsbh:
+      if (!is_csb_alg(f->alg)) return fail(kInvalidArgument, "format is not CSB");
+      return spmv_blocked(*f, x, y, s);
+    case kMergeB:
+    case kMergeBH:
+      if (!is_mergeb_alg(f->alg)) return fail(kInvalidArgument, "format is not MergeB");
+      return spmv_blocked(*f, x, y, s);
+    case kBcoh:
+    case kBcohc:
+    case kBcohch:
+    case kBcohchp:
+      if (!is_bcoh_alg(f->alg)) return fail(kInvalidArgument, "format is not BCOH");
+      if (p != f->bands)
+        return fail(kInvalidArgument, "matrix was built for " + std::to_string(f->bands) +
+                                          " bands, multiply requested " + std::to_string(p));
+      return spmv_blocked(*f, x, y, s);
+    default:
+      return fail(kInvalidArgument, "unknown algorithm");
+  }
+}
+
+int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const double* x_host,
+                               uint64_t x_len, double* y_host, uint64_t y_len, unsigned p,
+                               const spmvlab_cuda_options* opt, double* x_dev, double* y_dev,
+                               void* stream) {
+  if (!f) return fail(kInvalidArgument, "null format");
+  if (x_len != f->n || y_len != f->m) return spmvlab_cuda_run_spmv(alg, f, x_dev, x_len, y_dev, y_len, p, opt, stream);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (x_len) cudaMemcpyAsync(x_dev, x_host, x_len * sizeof(double), cudaMemcpyHostToDevice, s);
+  const int rc = spmvlab_cuda_run_spmv(alg, f, x_dev, x_len, y_dev, y_len, p, opt, stream);
+  if (rc) return rc;
+  if (y_len) cudaMemcpyAsync(y_host, y_dev, y_len * sizeof(double), cudaMemcpyDeviceToHost, s);
+  return check_launch("run_spmv_host");
+}
+
+int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,
+                                size_t capacity, size_t* count) {
+  if (!f) return fail(kInvalidArgument, "null format");
+  if (count) *count = (size_t)f->nstorage;
+  if (!rows) return kOk;
+  for (int i = 0; i < f->nstorage && (size_t)i < capacity; ++i) {
+    std::memset(rows[i].name, 0, sizeof(rows[i].name));
+    std::strncpy(rows[i].name, f->arrays[i].name.c_str(), sizeof(rows[i].name) - 1);
+    rows[i].bytes = f->arrays[i].bytes;
+  }
+  return kOk;
+}
+
+int spmvlab_cuda_get_format_info(const spmvlab_cuda_format* f, spmvlab_cuda_format_info* info) {
+  if (!f || !info) return fail(kInvalidArgument, "null argument");
+  info->alg = f->alg;
+  info->m = f->m;
+  info->n = f->n;
+  info->nnz = f->nnz;
+  info->log2_beta = f->log2_beta;
+  info->block_rows = f->block_rows;
+  info->block_cols = f->block_cols;
+  info->element_level = f->element_level;
+  info->block_level = f->block_level;
+  info->bands = f->bands;
+  info->merge_tiles = f->merge_tiles;
+  info->work_items = f->work_items;
+  return kOk;
+}
+
+int spmvlab_cuda_format_array(const spmvlab_cuda_format* f, const char* name, const void** dev_ptr,
+                              uint64_t* bytes) {
+  if (!f || !name) return fail(kInvalidArgument, "null argument");
+  const DevArray* a = f->find(name);
+  if (!a) return fail(kInvalidArgument, std::string("no array named ") + name);
+  if (dev_ptr) *dev_ptr = a->ptr;
+  if (bytes) *bytes = a->bytes;
+  return kOk;
+}
+
+int spmvlab_cuda_download_array(const spmvlab_cuda_format* f, const char* name, void* host_dst,
+                                uint64_t capacity, uint64_t* bytes) {
+  if (!f || !name) return fail(kInvalidArgument, "null argument");
+  const DevArray* a = f->find(name);
+  if (!a) return fail(kInvalidArgument, std::string("no array named ") + name);
+  if (bytes) *bytes = a->bytes;
+  if (!host_dst) return kOk;
+  if (capacity < a->bytes) return fail(kInvalidArgument, "host buffer too small");
+  if (a->bytes && cudaMemcpy(host_dst, a->ptr, a->bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return check_launch("download_array");
+  return kOk;
+}
+
+void spmvlab_cuda_free_format(spmvlab_cuda_format* f) { delete f; }
+
+int spmvlab_cuda_validate(const spmvlab_cuda_coo* a, void* stream) {
+  if (!a) return fail(kInvalidArgument, "null argument");
+  if ((uint64_t)a->m > (1ull << 31) || (uint64_t)a->n > (1ull << 31))
+    return fail(kOverflow, "matrix dimension exceeds the supported index width");
+  Arena ar(static_cast<cudaStream_t>(stream));
+  const int rc = validate_coo(*a, ar);
+  if (rc == kIndexOutOfRange) return fail(rc, "index out of range: entry outside the matrix shape");
+  if (rc == kDuplicateEntry) return fail(rc, "duplicate entry: duplicate (row, col) coordinate");
+  return rc;
+}
+
+int spmvlab_cuda_merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b,
+                                   uint64_t b_len, const uint64_t* diags, uint64_t count,
+                                   uint64_t* out_i, void* stream) {
+  return merge_path_search(a, a_len, b, b_len, diags, count, out_i, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_curve_keys(int kind, const uint32_t* rows, const uint32_t* cols, uint64_t count,
+                            unsigned level, uint64_t* keys, void* stream) {
+  if (level > 31) return fail(kInvalidArgument, "curve level exceeds 31");
+  return curve_keys(kind, rows, cols, count, level, keys, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_sort_pairs(uint64_t* keys, uint32_t* values, uint64_t count, int begin_bit,
+                            int end_bit, void* stream) {
+  if (begin_bit < 0 || end_bit > 64 || begin_bit > end_bit) return fail(kInvalidArgument, "bad bit range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Arena ar(s);
+  uint64_t* k2 = ar.alloc_n<uint64_t>(count);
+  uint32_t* v2 = ar.alloc_n<uint32_t>(count);
+  if (!k2 || !v2) return fail(kNoMemory, "device allocation failed");
+  if (radix_sort_pairs(keys, k2, values, v2, count, begin_bit, end_bit, ar)) {
+    cudaMemcpyAsync(keys, k2, count * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(values, v2, count * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  ar.release();
+  return check_launch("sort_pairs");
+}
+
+int spmvlab_cuda_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, void* stream) {
+  Arena ar(static_cast<cudaStream_t>(stream));
+  exclusive_scan_u32(in, out, n, ar);
+  ar.release();
+  return check_launch("exclusive_scan");
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// convert_crs.cu -- COO -> CRS (triplet_to_crs, inc/crs.hpp:67-91) and the merge-path tile plan.
+//
+// Reference: sort a permutation by (row, col) with a comparator, count rows, partial_sum, gather.
+// Here: one 64-bit key (row << colbits | col) per entry, LSD radix sort of (key, entry index) over
+// exactly bit_width(m-1) + bit_width(n-1) bits, then one populate pass that derives col_ind from
+// the key, gathers data through the permutation and histograms rows (warp-aggregated atomics over
+// the sorted, hence run-grouped, rows), and a decoupled look-back scan for row_ptr.  Keys are
+// unique, so the order -- and every output array -- is bit-identical to the reference's.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spmvcu {
+namespace {
+
+__global__ void crs_keys(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cols,
+                         uint64_t nnz, uint32_t m, uint32_t n, int colbits, uint64_t* __restrict__ keys,
+                         uint32_t* __restrict__ idx, uint32_t* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const uint32_t r = rows[k], c = cols[k];
+    if (r >= m || c >= n) atomicOr(err, 1u);
+    keys[k] = ((uint64_t)r << colbits) | c;
+    idx[k] = (uint32_t)k;
+  }
+}
+
+__global__ void crs_populate(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ perm,
+                             const double* __restrict__ vals, uint64_t nnz, int colbits,
+                             uint32_t* __restrict__ col_ind, double* __restrict__ data,
+                             uint32_t* __restrict__ counts, uint32_t* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t cmask = (colbits >= 64) ? ~0ull : ((1ull << colbits) - 1);
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const uint64_t key = skeys[k];
+    const uint32_t row = (uint32_t)(key >> colbits);
+    col_ind[k] = (uint32_t)(key & cmask);
+    data[k] = vals[perm[k]];
+    if (k > 0 && skeys[k - 1] == key) atomicOr(err, 2u);
+    const unsigned active = __activemask();
+    const unsigned peers = __match_any_sync(active, row);
+    if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&counts[row], (unsigned)__popc(peers));
+  }
+}
+
+// One merge-path diagonal per tile boundary (diagonal_search, spmv_parallel.hpp:47-69, with
+// A = row_ptr[1..m], B = 0..nnz-1).
+__global__ void merge_partition(const uint32_t* __restrict__ row_ptr, uint32_t m, uint64_t nnz,
+                                uint32_t tiles, uint32_t tile_items, uint32_t* __restrict__ trow,
+                                uint32_t* __restrict__ tnnz) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > tiles) return;
+  const uint64_t total = (uint64_t)m + nnz;
+  const uint64_t dt = (uint64_t)t * tile_items;
+  const uint64_t diag = dt < total ? dt : total;
+  uint64_t lo = diag > nnz ? diag - nnz : 0;
+  uint64_t hi = diag < m ? diag : m;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo + 1) / 2;
+    if ((uint64_t)row_ptr[mid] <= diag - mid) lo = mid; else hi = mid - 1;
+  }
+  trow[t] = (uint32_t)lo;
+  tnnz[t] = (uint32_t)(diag - lo);
+}
+
+__global__ void merge_path_search_kernel(const uint32_t* __restrict__ a, uint64_t a_len,
+                                         const uint32_t* __restrict__ b,
+                                         uint64_t b_len, const uint64_t* __restrict__ diags,
+                                         uint64_t count, uint64_t* __restrict__ out_i) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const uint64_t diag = diags[k];
+  uint64_t lo = diag > b_len ? diag - b_len : 0;
+  uint64_t hi = diag < a_len ? diag : a_len;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo + 1) / 2;
+    const uint64_t j = diag - mid;
+    const uint64_t bj = b ? (uint64_t)b[j < b_len ? j : 0] : j;
+    const bool pred = j >= b_len || !(bj < (uint64_t)a[mid - 1]);
+    if (pred) lo = mid; else hi = mid - 1;
+  }
+  out_i[k] = lo;
+}
+
+}  // namespace
+
+int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar) {
+  cudaStream_t s = ar.stream();
+  const uint64_t nnz = a.nnz;
+  uint32_t* row_ptr = static_cast<uint32_t*>(f.add("row_ptr", (uint64_t)a.m + 1, 4, s));
+  uint32_t* col_ind = static_cast<uint32_t*>(f.add("col_ind", nnz, 4, s));
+  double* data = static_cast<double*>(f.add("data", nnz, 8, s));
+  f.nstorage = 3;
+  if (!row_ptr || !col_ind || !data) return kNoMemory;
+  cudaMemsetAsync(row_ptr, 0, sizeof(uint32_t) * ((uint64_t)a.m + 1), s);
+  if (nnz == 0) return check_launch("build_crs");
+
+  const int colbits = (int)bit_width64(a.n > 0 ? a.n - 1 : 0);
+  const int rowbits = (int)bit_width64(a.m > 0 ? a.m - 1 : 0);
+  uint64_t* keys = ar.alloc_n<uint64_t>(nnz);
+  uint64_t* keys2 = ar.alloc_n<uint64_t>(nnz);
+  uint32_t* idx = ar.alloc_n<uint32_t>(nnz);
+  uint32_t* idx2 = ar.alloc_n<uint32_t>(nnz);
+  uint32_t* err = ar.alloc_n<uint32_t>(1);
+  if (!keys || !keys2 || !idx || !idx2 || !err) return kNoMemory;
+  cudaMemsetAsync(err, 0, 4, s);
+  crs_keys<<<grid_for(nnz, 256), 256, 0, s>>>(a.row_ind, a.col_ind, nnz, a.m, a.n, colbits, keys, idx, err);
+  const bool alt = radix_sort_pairs(keys, keys2, idx, idx2, nnz, 0, colbits + rowbits, ar);
+  const uint64_t* sk = alt ? keys2 : keys;
+  const uint32_t* sp = alt ? idx2 : idx;
+  crs_populate<<<grid_for(nnz, 256), 256, 0, s>>>(sk, sp, a.data, nnz, colbits, col_ind, data, row_ptr, err);
+  exclusive_scan_u32(row_ptr, row_ptr, a.m, ar);
+  uint32_t herr = 0;
+  cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_crs");
+  if (herr & 1u) return kIndexOutOfRange;
+  if (herr & 2u) return kDuplicateEntry;
+  return check_launch("build_crs");
+}
+
+int build_merge_plan(Format& f, Arena& ar) {
+  cudaStream_t s = ar.stream();
+  const uint64_t total = (uint64_t)f.m + f.nnz;
+  const uint64_t tiles = (total + kMergeTile - 1) / kMergeTile;
+  f.merge_tiles = (uint32_t)tiles;
+  uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + 1, 4, s));
+  uint32_t* tnnz = static_cast<uint32_t*>(f.add("merge_tile_nnz", tiles + 1, 4, s));
+  if (!f.add("merge_carry_row", tiles + 1, 4, s) || !f.add("merge_carry_val", tiles + 1, 8, s) || !trow || !tnnz)
+    return kNoMemory;
+  merge_partition<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, s>>>(
+      f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, kMergeTile, trow, tnnz);
+  // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32].
+  const double mean = f.m ? (double)f.nnz / f.m : 0.0;
+  uint32_t g = 2;
+  while (g < 32 && g < mean) g <<= 1;
+  f.par_group = g;
+  return check_launch("build_merge_plan");
+}
+
+int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,
+                      uint64_t count, uint64_t* out_i, cudaStream_t s) {
+  if (count == 0) return kOk;
+  merge_path_search_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(a, a_len, b, b_len, diags, count, out_i);
+  return check_launch("merge_path_search");
+}
+
+}  // namespace spmvcu

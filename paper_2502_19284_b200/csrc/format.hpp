@@ -1,0 +1,56 @@
+// format.hpp -- the device-resident format object behind the C ABI (include/spmvlab_cuda.h).
+//
+// A format is a list of named device arrays.  The first `nstorage` arrays are exactly the arrays
+// of the reference's storage_report() for that format (inc/storage.hpp:62-123), with identical
+// element widths and lengths, so storage_report() byte counts match the reference.  BCOH bands are
+// concatenated end to end; per-band slices are delimited by the auxiliary off_* tables.
+// Everything a multiply needs beyond the storage arrays (merge-path tile coordinates, carry slots,
+// block work queues) is built with the format, so the timed multiply allocates nothing.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+struct DevArray {
+  std::string name;
+  void* ptr = nullptr;
+  uint64_t bytes = 0;   // logical bytes (reported)
+  uint32_t esz = 0;
+  template <typename T>
+  T* as() const { return static_cast<T*>(ptr); }
+  uint64_t count() const { return esz ? bytes / esz : 0; }
+};
+
+struct spmvlab_cuda_format {
+  int alg = 0;
+  uint32_t m = 0, n = 0;
+  uint64_t nnz = 0;
+  uint32_t log2_beta = 0, block_rows = 0, block_cols = 0;
+  uint32_t element_level = 0, block_level = 0, bands = 0;
+  int nstorage = 0;
+  std::vector<DevArray> arrays;
+
+  // ---- merge-path plan (CRS formats), spmv_parallel.hpp:82-86 at tile granularity
+  uint32_t merge_tiles = 0;
+
+  // ---- ParCRS launch shape
+  uint32_t par_group = 32;
+
+  // ---- blocked plan (CSB / MergeB / BCOH): work items = (element range, y window)
+  uint32_t work_items = 0;
+  bool needs_zero_y = false;
+
+  ~spmvlab_cuda_format();
+  DevArray* find(const std::string& name);
+  const DevArray* find(const std::string& name) const;
+  // Allocates a named device array (16-byte padded); returns nullptr on failure.
+  void* add(const std::string& name, uint64_t count, uint32_t esz, cudaStream_t s);
+  void set_count(const std::string& name, uint64_t count);
+};
+
+namespace spmvcu {
+using Format = spmvlab_cuda_format;
+}

@@ -1,0 +1,44 @@
+// kernels.cuh -- host launchers for the conversions and the multiplies.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/spmvlab_cuda.h"
+#include "format.hpp"
+#include "primitives.cuh"
+
+namespace spmvcu {
+
+// merge-CSR tile geometry: THREADS x ITEMS merge items per CTA tile.
+constexpr int kMergeThreads = 256;
+constexpr int kMergeIpt = 8;
+constexpr int kMergeTile = kMergeThreads * kMergeIpt;
+
+// ---- conversions (COO -> format); each returns a Status
+int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar);
+int build_merge_plan(Format& f, Arena& ar);
+int build_csb(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, bool hilbert, uint64_t split_threshold, Arena& ar);
+int build_mergeb(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, bool hilbert, Arena& ar);
+int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, unsigned p, Arena& ar);
+
+// ---- multiplies (stream-ordered; y fully overwritten)
+int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s);
+int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s);
+int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s);
+int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s);
+
+// ---- primitives
+int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,
+                      uint64_t count, uint64_t* out_i, cudaStream_t s);
+int curve_keys(int kind, const uint32_t* rows, const uint32_t* cols, uint64_t count, unsigned level,
+               uint64_t* keys, cudaStream_t s);
+int validate_coo(const spmvlab_cuda_coo& a, Arena& ar);
+
+inline unsigned grid_for(uint64_t n, unsigned threads, unsigned max_blocks = kNumSMs * 16) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (unsigned)(b < max_blocks ? b : max_blocks);
+}
+
+}  // namespace spmvcu

@@ -1,0 +1,339 @@
+// primitives.cu -- radix sort and scan for the COO->format conversions (sm_100a).
+//
+// The reference sorts a permutation with a comparator (parallel_chunk_sort, inc/parallel.hpp:72-97)
+// and recomputes curve ranks inside every comparison (inc/csb.hpp:77-78, inc/bcoh.hpp:240-246).
+// Here every conversion first materialises one unique 64-bit key per entry and then sorts
+// (key, entry index) pairs with an LSD radix sort: one "onesweep" kernel per 8-bit digit, each
+// reading and writing the pairs exactly once, tile prefixes resolved by decoupled look-back.
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "primitives.cuh"
+
+namespace spmvcu {
+
+extern thread_local std::string g_last_error;
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return kCudaError;
+  }
+  return kOk;
+}
+
+void* Arena::alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s_) != cudaSuccess) return nullptr;
+  ptrs_.push_back(p);
+  return p;
+}
+
+void Arena::release() {
+  for (void* p : ptrs_) cudaFreeAsync(p, s_);
+  ptrs_.clear();
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kIpt = 16;
+constexpr int kTile = kThreads * kIpt;  // 4096 pairs per tile
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPrefix = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back over one 64-bit status word per (tile, lane-slot): returns the exclusive
+// prefix of `count` over all earlier tiles and publishes the inclusive prefix.
+__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, uint32_t slot,
+                                             uint32_t slots, uint64_t count) {
+  uint64_t* mine = status + (uint64_t)tile * slots + slot;
+  if (tile == 0) {
+    st_relaxed(mine, kFlagPrefix | count);
+    return 0;
+  }
+  st_relaxed(mine, kFlagAgg | count);
+  uint64_t excl = 0;
+  int64_t t = (int64_t)tile - 1;
+  while (true) {
+    const uint64_t v = ld_relaxed(status + (uint64_t)t * slots + slot);
+    const uint64_t flag = v & ~kValMask;
+    if (flag == 0) continue;  // predecessor not published yet
+    excl += v & kValMask;
+    if (flag == kFlagPrefix) break;
+    --t;
+  }
+  st_relaxed(mine, kFlagPrefix | (excl + count));
+  return excl;
+}
+
+// ------------------------------------------------------------------ radix sort
+
+__global__ void __launch_bounds__(kThreads) rs_histogram(const uint64_t* __restrict__ keys, uint64_t n,
+                                                         int begin_bit, int end_bit, int npasses,
+                                                         uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8 * 256];
+  for (int i = threadIdx.x; i < npasses * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += stride) {
+    const uint64_t key = keys[idx];
+    const unsigned active = __activemask();
+    for (int p = 0; p < npasses; ++p) {
+      const int shift = begin_bit + 8 * p;
+      const int bits = min(8, end_bit - shift);
+      const unsigned d = (unsigned)(key >> shift) & ((1u << bits) - 1u);
+      const unsigned peers = __match_any_sync(active, d);
+      if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&sh[p * 256 + d], (unsigned)__popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npasses * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// hist[p][d] -> exclusive offsets over d, in place.  One block per pass.
+__global__ void rs_hist_scan(uint32_t* hist) {
+  __shared__ uint32_t s[256];
+  uint32_t* h = hist + blockIdx.x * 256;
+  s[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int d = 0; d < 256; ++d) {
+      const uint32_t c = s[d];
+      s[d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  h[threadIdx.x] = s[threadIdx.x];
+}
+
+constexpr size_t kOnesweepSmem =
+    sizeof(uint64_t) * kTile + sizeof(uint32_t) * kTile + sizeof(uint32_t) * kWarps * 256 +
+    sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
+
+__global__ void __launch_bounds__(kThreads) rs_onesweep(
+    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t dmask,
+    const uint32_t* __restrict__ pass_offset, uint64_t* status, uint32_t* tile_counter) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kTile);
+  uint32_t* s_whist = s_vals + kTile;          // [warp][digit]
+  uint32_t* s_local = s_whist + kWarps * 256;  // tile-local exclusive digit offsets
+  int64_t* s_gbase = reinterpret_cast<int64_t*>(s_local + 256);
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_wsum[kWarps];
+
+  const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < kWarps * 256; i += kThreads) s_whist[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kTile;
+  const uint64_t wbase = base + (uint64_t)warp * (kIpt * 32);
+
+  uint64_t key[kIpt];
+  uint32_t val[kIpt];
+  uint32_t rank[kIpt];
+#pragma unroll
+  for (int i = 0; i < kIpt; ++i) {
+    const uint64_t idx = wbase + i * 32 + lane;
+    if (idx < n) {
+      key[i] = kin[idx];
+      val[i] = vin[idx];
+    }
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kIpt; ++i) {
+    const uint64_t idx = wbase + i * 32 + lane;
+    const bool valid = idx < n;
+    const unsigned d = valid ? ((unsigned)(key[i] >> shift) & dmask) : (0x100u + lane);
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+    uint32_t prior = 0;
+    if (valid) {
+      prior = s_whist[warp * 256 + d];
+      rank[i] = prior + __popc(peers & lt_mask);
+    }
+    __syncwarp();
+    if (valid && lane == (unsigned)(__ffs(peers) - 1)) s_whist[warp * 256 + d] = prior + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // per digit (one thread each): warp prefix, tile count, tile-local offset, global base
+  const unsigned d = tid;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t c = s_whist[w * 256 + d];
+    s_whist[w * 256 + d] = cnt;
+    cnt += c;
+  }
+  // block-exclusive scan of cnt over digits
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= (unsigned)off) incl += t;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (unsigned w = 0; w < warp; ++w) wpre += s_wsum[w];
+  const uint32_t local_excl = wpre + incl - cnt;
+  s_local[d] = local_excl;
+  const uint64_t excl = lookback(status, tile, d, 256, cnt);
+  s_gbase[d] = (int64_t)pass_offset[d] + (int64_t)excl - (int64_t)local_excl;
+  __syncthreads();
+
+#pragma unroll
+  for (int i = 0; i < kIpt; ++i) {
+    const uint64_t idx = wbase + i * 32 + lane;
+    if (idx < n) {
+      const unsigned dd = (unsigned)(key[i] >> shift) & dmask;
+      const uint32_t pos = s_local[dd] + s_whist[warp * 256 + dd] + rank[i];
+      s_keys[pos] = key[i];
+      s_vals[pos] = val[i];
+    }
+  }
+  __syncthreads();
+  const uint32_t valid_n = (n - base) < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
+  for (uint32_t j = tid; j < valid_n; j += kThreads) {
+    const uint64_t k = s_keys[j];
+    const unsigned dd = (unsigned)(k >> shift) & dmask;
+    const uint64_t o = (uint64_t)(s_gbase[dd] + (int64_t)j);
+    kout[o] = k;
+    vout[o] = s_vals[j];
+  }
+}
+
+// ------------------------------------------------------------------ exclusive scan
+
+__device__ __forceinline__ unsigned pad_idx(unsigned i) { return i + (i >> 5); }
+
+__global__ void __launch_bounds__(kThreads) scan_u32(const uint32_t* in, uint32_t* out, uint64_t n,
+                                                     uint64_t* status, uint32_t* tile_counter) {
+  __shared__ uint32_t s[kTile + kTile / 32];
+  __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_excl;
+  const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kTile;
+#pragma unroll
+  for (int i = 0; i < kIpt; ++i) {
+    const unsigned li = i * kThreads + tid;
+    const uint64_t idx = base + li;
+    s[pad_idx(li)] = idx < n ? in[idx] : 0u;
+  }
+  __syncthreads();
+  uint32_t v[kIpt];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    v[k] = s[pad_idx(tid * kIpt + k)];
+    sum += v[k];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= (unsigned)off) incl += t;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, total = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if ((unsigned)w < warp) wpre += s_wsum[w];
+    total += s_wsum[w];
+  }
+  if (tid == 0) s_excl = lookback(status, tile, 0, 1, total);
+  __syncthreads();
+  uint32_t run = (uint32_t)s_excl + wpre + incl - sum;
+#pragma unroll
+  for (int k = 0; k < kIpt; ++k) {
+    s[pad_idx(tid * kIpt + k)] = run;
+    run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kIpt; ++i) {
+    const unsigned li = i * kThreads + tid;
+    const uint64_t idx = base + li;
+    if (idx < n) out[idx] = s[pad_idx(li)];
+  }
+  if (base + kTile >= n && tid == 0) out[n] = (uint32_t)(s_excl + total);
+}
+
+}  // namespace
+
+bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
+                      uint64_t n, int begin_bit, int end_bit, Arena& arena) {
+  if (n <= 1 || end_bit <= begin_bit) return false;
+  cudaStream_t s = arena.stream();
+  const int npasses = (end_bit - begin_bit + 7) / 8;
+  uint32_t* hist = arena.alloc_n<uint32_t>(npasses * 256);
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * npasses * 256, s);
+  const int hblocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)kNumSMs * 8);
+  rs_histogram<<<hblocks, 256, 0, s>>>(keys, n, begin_bit, end_bit, npasses, hist);
+  rs_hist_scan<<<npasses, 256, 0, s>>>(hist);
+
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  uint64_t* status = arena.alloc_n<uint64_t>(tiles * 256 + 8);
+  uint32_t* counter = reinterpret_cast<uint32_t*>(status + tiles * 256);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOnesweepSmem);
+    attr_set = true;
+  }
+  bool in_alt = false;
+  for (int p = 0; p < npasses; ++p) {
+    const int shift = begin_bit + 8 * p;
+    const int bits = std::min(8, end_bit - shift);
+    cudaMemsetAsync(status, 0, sizeof(uint64_t) * (tiles * 256 + 8), s);
+    const uint64_t* ki = in_alt ? keys_alt : keys;
+    const uint32_t* vi = in_alt ? vals_alt : vals;
+    uint64_t* ko = in_alt ? keys : keys_alt;
+    uint32_t* vo = in_alt ? vals : vals_alt;
+    rs_onesweep<<<(unsigned)tiles, kThreads, kOnesweepSmem, s>>>(ki, vi, ko, vo, n, shift,
+                                                                (1u << bits) - 1u, hist + p * 256,
+                                                                status, counter);
+    in_alt = !in_alt;
+  }
+  return in_alt;
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, Arena& arena) {
+  cudaStream_t s = arena.stream();
+  if (n == 0) {
+    cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
+    return;
+  }
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  uint64_t* status = arena.alloc_n<uint64_t>(tiles + 8);
+  cudaMemsetAsync(status, 0, sizeof(uint64_t) * (tiles + 8), s);
+  scan_u32<<<(unsigned)tiles, kThreads, 0, s>>>(in, out, n, status,
+                                                reinterpret_cast<uint32_t*>(status + tiles));
+}
+
+}  // namespace spmvcu

@@ -1,0 +1,323 @@
+"""Python mirror of the reference's algorithm interface (inc/engine.hpp) over the CUDA C ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+
+  * ``Algorithm`` / ``all_algorithms`` / ``algorithm_name`` / ``algorithm_from_name``
+    (inc/engine.hpp:30-72)
+  * ``EngineOptions`` (inc/engine.hpp:75-79)
+  * ``build_format(alg, a, threads, opt)`` (inc/engine.hpp:96-122) -> ``BuiltFormat``
+  * ``run_spmv(alg, format, x, y, p, opt)`` (inc/engine.hpp:126-156); y fully overwritten
+  * ``storage_report(format)`` (inc/engine.hpp:158-160, inc/storage.hpp:38-123)
+  * ``validate(a)`` (inc/triplet.hpp:42-59)
+  * ``Error`` carrying an ``ErrorKind`` (inc/types.hpp:47-104)
+
+Matrices and vectors live in device memory as torch tensors (torch is only the allocator and
+stream provider here); every computation runs in libspmvlab_cuda.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import capi
+
+
+class Algorithm(enum.IntEnum):
+    SeqCrs = 0
+    ParCrs = 1
+    Merge = 2
+    Csb = 3
+    Csbh = 4
+    Bcoh = 5
+    Bcohc = 6
+    Bcohch = 7
+    Bcohchp = 8
+    MergeB = 9
+    MergeBH = 10
+
+
+all_algorithms = tuple(Algorithm)
+_NAMES = ["crs", "parcrs", "merge", "csb", "csbh", "bcoh", "bcohc", "bcohch", "bcohchp", "mergeb",
+          "mergebh"]
+
+
+def algorithm_name(alg) -> str:
+    return _NAMES[int(alg)]
+
+
+def algorithm_from_name(name: str) -> Algorithm:
+    if name in _NAMES:
+        return Algorithm(_NAMES.index(name))
+    raise Error(ErrorKind.InvalidArgument, f"unknown algorithm '{name}'")
+
+
+class ErrorKind(enum.IntEnum):
+    DimensionMismatch = 0
+    InvalidArgument = 1
+    CorruptFormat = 2
+    Overflow = 3
+    BadHeader = 4
+    UnsupportedFormat = 5
+    UnsupportedField = 6
+    UnsupportedSymmetry = 7
+    IndexOutOfRange = 8
+    DuplicateEntry = 9
+    ParseError = 10
+    Truncated = 11
+    BadMagic = 12
+    IoError = 13
+
+
+class Error(RuntimeError):
+    """spmvlab::Error (inc/types.hpp:86-96)."""
+
+    def __init__(self, kind: ErrorKind, message: str):
+        super().__init__(f"{kind.name}: {message}")
+        self.kind = kind
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = capi.load().spmvlab_cuda_last_error().decode(errors="replace")
+    if rc < 100:
+        raise Error(ErrorKind(rc - 1), msg)
+    raise CudaError(f"CUDA failure {rc}: {msg}")
+
+
+DEFAULT_L2_BYTES = 512 * 1024  # inc/block_size.hpp:39
+
+
+@dataclass
+class EngineOptions:
+    l2_bytes: int = DEFAULT_L2_BYTES
+    split_threshold: int = 0
+    build_threads: int = 1
+
+    def _c(self) -> capi.Options:
+        return capi.Options(self.l2_bytes, self.split_threshold, self.build_threads)
+
+
+@dataclass
+class TripletMatrix:
+    """Device-resident COO (inc/triplet.hpp:30-38): int32-typed u32 indices, float64 data."""
+    m: int
+    n: int
+    row_ind: torch.Tensor
+    col_ind: torch.Tensor
+    data: torch.Tensor
+
+    def nnz(self) -> int:
+        return int(self.data.numel())
+
+    @staticmethod
+    def from_host(m, n, rows, cols, vals, device="cuda") -> "TripletMatrix":
+        r = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.uint32).view(np.int32)).to(device)
+        c = torch.from_numpy(np.ascontiguousarray(cols, dtype=np.uint32).view(np.int32)).to(device)
+        v = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)).to(device)
+        return TripletMatrix(int(m), int(n), r, c, v)
+
+    def _c(self) -> capi.Coo:
+        for t in (self.row_ind, self.col_ind, self.data):
+            if self.nnz() and (not t.is_cuda or not t.is_contiguous()):
+                raise Error(ErrorKind.InvalidArgument, "triplet arrays must be contiguous CUDA tensors")
+        if not (self.row_ind.numel() == self.col_ind.numel() == self.data.numel()):
+            raise Error(ErrorKind.InvalidArgument, "triplet arrays must have equal length")
+        if self.data.dtype != torch.float64:
+            raise Error(ErrorKind.InvalidArgument, "triplet data must be float64")
+        return capi.Coo(self.m, self.n, self.nnz(), self.row_ind.data_ptr(), self.col_ind.data_ptr(),
+                        self.data.data_ptr())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+@dataclass
+class StorageArray:
+    name: str
+    bytes: int
+
+
+@dataclass
+class StorageBreakdown:
+    """inc/storage.hpp:38-55."""
+    format: str
+    arrays: list = field(default_factory=list)
+
+    def bytes(self, name: str) -> int:
+        return sum(a.bytes for a in self.arrays if a.name == name)
+
+    def total(self) -> int:
+        return sum(a.bytes for a in self.arrays)
+
+    def index_bytes(self) -> int:
+        return self.total() - self.bytes("data")
+
+
+_DT = {"data": np.float64, "row_jump_block": np.int16, "col_jump_block": np.int16,
+       "col_inc": np.uint16, "row_jump": np.uint16, "merge_carry_val": np.float64}
+_U64 = {"off_elem", "off_block", "off_row_jump_block", "off_blk_ptr", "off_row_jump"}
+
+
+class BuiltFormat:
+    """A device-resident format (the BuiltFormat variant, inc/engine.hpp:82)."""
+
+    def __init__(self, handle: int, alg: Algorithm):
+        self._h = C.c_void_p(handle)
+        self.alg = Algorithm(alg)
+        info = capi.FormatInfo()
+        _check(capi.load().spmvlab_cuda_get_format_info(self._h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in capi.FormatInfo._fields_}
+        self.m, self.n, self.nnz_ = info.m, info.n, info.nnz
+
+    def nnz(self) -> int:
+        return int(self.nnz_)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def array(self, name: str) -> np.ndarray:
+        """Synchronous host copy of one named array (parity downloads)."""
+        L = capi.load()
+        nbytes = C.c_uint64()
+        _check(L.spmvlab_cuda_download_array(self._h, name.encode(), None, 0, C.byref(nbytes)))
+        dt = np.uint64 if name in _U64 else _DT.get(name, np.uint32)
+        out = np.zeros(nbytes.value // np.dtype(dt).itemsize, dtype=dt)
+        if out.size:
+            _check(L.spmvlab_cuda_download_array(self._h, name.encode(), out.ctypes.data, out.nbytes,
+                                                 C.byref(nbytes)))
+        return out
+
+    def close(self):
+        if self._h:
+            try:
+                capi.load().spmvlab_cuda_free_format(self._h)
+            except Exception:
+                pass
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        self.close()
+
+
+def build_format(alg, a: TripletMatrix, threads: int = 1, opt: EngineOptions | None = None,
+                 stream=None) -> BuiltFormat:
+    """inc/engine.hpp:96-122 (COO -> format on the device)."""
+    opt = opt or EngineOptions()
+    h = C.c_void_p()
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_build_format(int(alg), C.byref(coo), int(threads), C.byref(opt._c()),
+                                                 C.byref(h), _stream(stream)))
+    return BuiltFormat(h.value, alg)
+
+
+def run_spmv(alg, fmt: BuiltFormat, x: torch.Tensor, y: torch.Tensor | None = None, p: int = 1,
+             opt: EngineOptions | None = None, stream=None) -> torch.Tensor:
+    """inc/engine.hpp:126-156: y = A x on the device (stream-ordered; y fully overwritten)."""
+    if y is None:
+        y = torch.empty(fmt.m, dtype=torch.float64, device=x.device)
+    if x.dtype != torch.float64 or y.dtype != torch.float64:
+        raise Error(ErrorKind.InvalidArgument, "x and y must be float64")
+    c_opt = (opt or EngineOptions())._c()
+    _check(capi.load().spmvlab_cuda_run_spmv(int(alg), fmt.handle, x.data_ptr(), x.numel(), y.data_ptr(),
+                                             y.numel(), int(p), C.byref(c_opt), _stream(stream)))
+    return y
+
+
+def run_spmv_host(alg, fmt: BuiltFormat, x_host: torch.Tensor, y_host: torch.Tensor, p: int,
+                  x_dev: torch.Tensor, y_dev: torch.Tensor, opt: EngineOptions | None = None,
+                  stream=None) -> torch.Tensor:
+    """Host-buffer multiply through the C ABI: H2D x, multiply, D2H y on one stream."""
+    c_opt = (opt or EngineOptions())._c()
+    _check(capi.load().spmvlab_cuda_run_spmv_host(int(alg), fmt.handle, x_host.data_ptr(), x_host.numel(),
+                                                  y_host.data_ptr(), y_host.numel(), int(p), C.byref(c_opt),
+                                                  x_dev.data_ptr(), y_dev.data_ptr(), _stream(stream)))
+    return y_host
+
+
+_FORMAT_NAMES = {0: "crs", 1: "crs", 2: "crs", 3: "csb", 4: "csbh", 5: "bcoh", 6: "bcohc", 7: "bcohch",
+                 8: "bcohchp", 9: "mergeb", 10: "mergebh"}
+
+
+def storage_report(fmt: BuiltFormat) -> StorageBreakdown:
+    """inc/engine.hpp:158-160."""
+    L = capi.load()
+    rows = (capi.StorageArray * 16)()
+    cnt = C.c_size_t()
+    _check(L.spmvlab_cuda_storage_report(fmt.handle, rows, 16, C.byref(cnt)))
+    return StorageBreakdown(_FORMAT_NAMES[int(fmt.alg)],
+                            [StorageArray(rows[i].name.decode(), int(rows[i].bytes)) for i in range(cnt.value)])
+
+
+def validate(a: TripletMatrix, stream=None) -> None:
+    """inc/triplet.hpp:42-59."""
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_validate(C.byref(coo), _stream(stream)))
+
+
+def select_block_size(n: int, index_bits_cap: int, l2_bytes: int = DEFAULT_L2_BYTES) -> int:
+    """inc/block_size.hpp:47-61 -> log2(beta)."""
+    return int(capi.load().spmvlab_cuda_select_block_size(n, index_bits_cap, l2_bytes))
+
+
+def engine_block_size(alg, n: int, opt: EngineOptions | None = None) -> int:
+    """inc/engine.hpp:84-91 -> log2(beta)."""
+    opt = opt or EngineOptions()
+    cap = 15 if Algorithm(alg) in (Algorithm.Bcoh, Algorithm.Bcohc, Algorithm.Bcohch, Algorithm.Bcohchp) else 16
+    return select_block_size(max(n, 1), cap, opt.l2_bytes)
+
+
+def partition_rows_by_nnz(prefix, p: int, log2_beta: int) -> np.ndarray:
+    """inc/block_size.hpp:73-102 (host)."""
+    prefix = np.ascontiguousarray(prefix, dtype=np.uint32)
+    out = np.zeros(p + 1, dtype=np.uint32)
+    _check(capi.load().spmvlab_cuda_partition_rows_by_nnz(prefix.ctypes.data, len(prefix) - 1, p, log2_beta,
+                                                          out.ctypes.data))
+    return out
+
+
+def merge_path_search(a: torch.Tensor, b, diags: torch.Tensor, stream=None) -> torch.Tensor:
+    """diagonal_search (inc/spmv_parallel.hpp:47-69) for many diagonals.  ``b`` is either a device
+    tensor (list B) or an int b_len meaning B[j] = j (the CRS merge path)."""
+    out = torch.empty(diags.numel(), dtype=torch.int64, device=a.device)
+    if isinstance(b, int):
+        bp, blen = None, b
+    else:
+        bp, blen = b.data_ptr(), b.numel()
+    _check(capi.load().spmvlab_cuda_merge_path_search(a.data_ptr(), a.numel(), bp, blen, diags.data_ptr(),
+                                                      diags.numel(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def curve_keys(kind: int, rows: torch.Tensor, cols: torch.Tensor, level: int, stream=None) -> torch.Tensor:
+    """Morton (kind 0) / Hilbert (kind 1) ranks on the device (inc/curves.hpp:107-143)."""
+    out = torch.empty(rows.numel(), dtype=torch.int64, device=rows.device)
+    _check(capi.load().spmvlab_cuda_curve_keys(kind, rows.data_ptr(), cols.data_ptr(), rows.numel(), level,
+                                               out.data_ptr(), _stream(stream)))
+    return out
+
+
+def sort_pairs(keys: torch.Tensor, values: torch.Tensor, begin_bit: int, end_bit: int, stream=None):
+    """In-place stable LSD radix sort of (u64 key, u32 value) pairs."""
+    _check(capi.load().spmvlab_cuda_sort_pairs(keys.data_ptr(), values.data_ptr(), keys.numel(), begin_bit,
+                                               end_bit, _stream(stream)))
+    return keys, values
+
+
+def exclusive_scan(counts: torch.Tensor, stream=None) -> torch.Tensor:
+    out = torch.empty(counts.numel() + 1, dtype=torch.int32, device=counts.device)
+    _check(capi.load().spmvlab_cuda_exclusive_scan(counts.data_ptr(), out.data_ptr(), counts.numel(),
+                                                   _stream(stream)))
+    return out
