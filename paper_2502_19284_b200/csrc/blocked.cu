@@ -1,25 +1,131 @@
-// blocked.cu -- CSB / MergeB / BCOH conversions and multiplies (placeholder until implemented).
+// blocked.cu -- the CSB / MergeB / BCOH multiplies on the device (sm_100a).
+//
+// Reference engines: spmv_csb (inc/spmv_parallel.hpp:202-331), spmv_bcoh (:336-350, replaying
+// bcoh_for_each_block / bcoh_for_each_element, inc/bcoh.hpp:115-187) and spmv_mergeb (:355-402).
+// All three walk an element stream that is grouped by sparse block, with in-block coordinates
+// either packed (row << 16 | col) or ICRS-compressed (u16 column increments that overflow at beta
+// into a u16 row jump).  On the GPU the block level is replaced by the absolute block table built
+// with the format (the BICRS / Hilbert-pointer decode pre-pass) and the stream is cut into chunks
+// of <= 256 elements that never cross a block.  One warp multiplies one chunk 32 elements at a
+// time: coalesced loads of the in-block indices and values, x gathers through the read-only path,
+// ICRS decoded with two warp prefix sums (in_col = S mod beta, row changes = S / beta, the row
+// jumps of the new rows summed with a second scan), a warp segmented reduction over runs of equal
+// rows, and one fp64 reduction into y per run (y is cleared first, as the reference engines clear
+// their output rows, spmv_parallel.hpp:277-281 and :344-345).
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace spmvcu {
+
 extern thread_local std::string g_last_error;
 
-int build_csb(Format&, const spmvlab_cuda_coo&, unsigned, bool, uint64_t, Arena&) {
-  g_last_error = "csb not implemented yet";
-  return kInvalidArgument;
+namespace {
+
+template <bool ICRS>
+__global__ void __launch_bounds__(256) blocked_spmv_kernel(
+    const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc,
+    const uint16_t* __restrict__ row_jump, const double* __restrict__ data,
+    const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
+    const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc, uint32_t nchunks, unsigned lb,
+    const double* __restrict__ x, double* __restrict__ y) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t mask = (1u << lb) - 1u;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  for (uint64_t c = gw; c < nchunks; c += nw) {
+    const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
+    const uint2 rc = blk_rc[ch_blk[c]];
+    const uint32_t rbase = rc.x << lb, cbase = rc.y << lb;
+    uint32_t S = 0, IR = 0, rjn = 0;
+    int R = -1;
+    if (ICRS) {
+      const uint4 st = ch_state[c];
+      S = st.x;
+      R = (int)st.y;
+      IR = st.z;
+      rjn = st.w;
+    }
+    for (uint32_t base = e0; base < e1; base += 32) {
+      const uint32_t k = base + lane;
+      const bool valid = k < e1;
+      uint32_t ir, ic;
+      if (!ICRS) {
+        const uint32_t pk = valid ? ld_stream(packed + k, pf) : 0u;
+        ir = pk >> 16;
+        ic = pk & 0xFFFFu;
+      } else {
+        uint32_t inc = valid ? (uint32_t)__ldg(col_inc + k) : 0u;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+          if ((int)lane >= off) inc += t;
+        }
+        const uint32_t Sk = S + inc;
+        const int r = (int)(Sk >> lb);
+        ic = Sk & mask;
+        const int r_last = __shfl_sync(0xFFFFFFFFu, r, 31);
+        const int nnew = r_last - R;
+        uint32_t jv = (int)lane < nnew ? (uint32_t)__ldg(row_jump + rjn + lane) : 0u;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, jv, off);
+          if ((int)lane >= off) jv += t;
+        }
+        const int idx = r - R - 1;
+        const uint32_t cum = __shfl_sync(0xFFFFFFFFu, jv, idx > 0 ? idx : 0);
+        ir = idx >= 0 ? IR + cum : IR;
+        S = __shfl_sync(0xFFFFFFFFu, Sk, 31);
+        IR = __shfl_sync(0xFFFFFFFFu, ir, 31);
+        R = r_last;
+        rjn += (uint32_t)nnew;
+      }
+      double v = valid ? ld_stream(data + k, pf) * ld_x(x + cbase + ic, pl) : 0.0;
+      const uint32_t row = valid ? rbase + ir : 0xFFFFFFFFu;
+      // warp segmented sum over runs of equal rows
+      const uint32_t prow = __shfl_up_sync(0xFFFFFFFFu, row, 1);
+      const unsigned heads = __ballot_sync(0xFFFFFFFFu, lane == 0 || prow != row);
+      const int seg_start = 31 - __clz(heads & (lt | (1u << lane)));
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double t = __shfl_up_sync(0xFFFFFFFFu, v, off);
+        if ((int)lane - off >= seg_start) v += t;
+      }
+      const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+      if (tail && valid) atomicAdd(y + row, v);
+    }
+  }
 }
-int build_mergeb(Format&, const spmvlab_cuda_coo&, unsigned, bool, Arena&) {
-  g_last_error = "mergeb not implemented yet";
-  return kInvalidArgument;
-}
-int build_bcoh(Format&, const spmvlab_cuda_coo&, unsigned, unsigned, Arena&) {
-  g_last_error = "bcoh not implemented yet";
-  return kInvalidArgument;
-}
-int spmv_blocked(const Format&, const double*, double*, cudaStream_t) {
-  g_last_error = "blocked not implemented yet";
-  return kInvalidArgument;
+
+}  // namespace
+
+int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
+  if (f.m) cudaMemsetAsync(y, 0, sizeof(double) * f.m, s);
+  if (f.work_items == 0) return check_launch("spmv_blocked");
+  const bool icrs = f.alg == kBcoh;
+  int dev = 0, sms = kNumSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t warps_needed = f.work_items;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((warps_needed + 7) / 8, (uint64_t)sms * 8);
+  const DevArray* pk = f.find("packed");
+  const DevArray* ci = f.find("col_inc");
+  const DevArray* rj = f.find("row_jump");
+  const DevArray* cs = f.find("chunk_state");
+  if (icrs)
+    blocked_spmv_kernel<true><<<blocks, 256, 0, s>>>(
+        nullptr, ci->as<uint16_t>(), rj->as<uint16_t>(), f.find("data")->as<double>(),
+        f.find("chunk_begin")->as<uint32_t>(), f.find("chunk_blk")->as<uint32_t>(), cs->as<uint4>(),
+        f.find("blk_rc")->as<uint2>(), f.work_items, f.log2_beta, x, y);
+  else
+    blocked_spmv_kernel<false><<<blocks, 256, 0, s>>>(
+        pk->as<uint32_t>(), nullptr, nullptr, f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
+        f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), f.work_items, f.log2_beta, x,
+        y);
+  return check_launch("spmv_blocked");
 }
 
 }  // namespace spmvcu

@@ -92,8 +92,8 @@ void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t
   a.name = name;
   a.esz = esz;
   a.bytes = count * esz;
-  // 16-byte padded so vector / bulk loads may over-read the tail safely.
-  const uint64_t alloc = ((a.bytes + 15) & ~uint64_t(15)) + 16;
+  // Padded so 16-byte-aligned bulk (TMA) copies may over-read up to 3 elements past the end.
+  const uint64_t alloc = ((a.bytes + 15) & ~uint64_t(15)) + 64;
   if (cudaMalloc(&a.ptr, alloc) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;

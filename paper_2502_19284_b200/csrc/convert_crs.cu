@@ -6,6 +6,9 @@
 // the key, gathers data through the permutation and histograms rows (warp-aggregated atomics over
 // the sorted, hence run-grouped, rows), and a decoupled look-back scan for row_ptr.  Keys are
 // unique, so the order -- and every output array -- is bit-identical to the reference's.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -13,19 +16,20 @@ namespace spmvcu {
 namespace {
 
 __global__ void crs_keys(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cols,
-                         uint64_t nnz, uint32_t m, uint32_t n, int colbits, uint64_t* __restrict__ keys,
-                         uint32_t* __restrict__ idx, uint32_t* err) {
+                         const double* __restrict__ vals, uint64_t nnz, uint32_t m, uint32_t n,
+                         int colbits, uint64_t* __restrict__ keys, uint64_t* __restrict__ payload,
+                         uint32_t* err) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
     const uint32_t r = rows[k], c = cols[k];
     if (r >= m || c >= n) atomicOr(err, 1u);
     keys[k] = ((uint64_t)r << colbits) | c;
-    idx[k] = (uint32_t)k;
+    payload[k] = __double_as_longlong(vals[k]);
   }
 }
 
-__global__ void crs_populate(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ perm,
-                             const double* __restrict__ vals, uint64_t nnz, int colbits,
+__global__ void crs_populate(const uint64_t* __restrict__ skeys, const uint64_t* __restrict__ svals,
+                             uint64_t nnz, int colbits,
                              uint32_t* __restrict__ col_ind, double* __restrict__ data,
                              uint32_t* __restrict__ counts, uint32_t* err) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -35,7 +39,7 @@ __global__ void crs_populate(const uint64_t* __restrict__ skeys, const uint32_t*
     const uint64_t key = skeys[k];
     const uint32_t row = (uint32_t)(key >> colbits);
     col_ind[k] = (uint32_t)(key & cmask);
-    data[k] = vals[perm[k]];
+    data[k] = __longlong_as_double((long long)svals[k]);
     if (k > 0 && skeys[k - 1] == key) atomicOr(err, 2u);
     const unsigned active = __activemask();
     const unsigned peers = __match_any_sync(active, row);
@@ -99,16 +103,17 @@ int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar) {
   const int rowbits = (int)bit_width64(a.m > 0 ? a.m - 1 : 0);
   uint64_t* keys = ar.alloc_n<uint64_t>(nnz);
   uint64_t* keys2 = ar.alloc_n<uint64_t>(nnz);
-  uint32_t* idx = ar.alloc_n<uint32_t>(nnz);
-  uint32_t* idx2 = ar.alloc_n<uint32_t>(nnz);
+  uint64_t* pay = ar.alloc_n<uint64_t>(nnz);
+  uint64_t* pay2 = ar.alloc_n<uint64_t>(nnz);
   uint32_t* err = ar.alloc_n<uint32_t>(1);
-  if (!keys || !keys2 || !idx || !idx2 || !err) return kNoMemory;
+  if (!keys || !keys2 || !pay || !pay2 || !err) return kNoMemory;
   cudaMemsetAsync(err, 0, 4, s);
-  crs_keys<<<grid_for(nnz, 256), 256, 0, s>>>(a.row_ind, a.col_ind, nnz, a.m, a.n, colbits, keys, idx, err);
-  const bool alt = radix_sort_pairs(keys, keys2, idx, idx2, nnz, 0, colbits + rowbits, ar);
+  crs_keys<<<grid_for(nnz, 256), 256, 0, s>>>(a.row_ind, a.col_ind, a.data, nnz, a.m, a.n, colbits, keys,
+                                              pay, err);
+  const bool alt = radix_sort_pairs(keys, keys2, pay, pay2, nnz, 0, colbits + rowbits, ar);
   const uint64_t* sk = alt ? keys2 : keys;
-  const uint32_t* sp = alt ? idx2 : idx;
-  crs_populate<<<grid_for(nnz, 256), 256, 0, s>>>(sk, sp, a.data, nnz, colbits, col_ind, data, row_ptr, err);
+  const uint64_t* sp = alt ? pay2 : pay;
+  crs_populate<<<grid_for(nnz, 256), 256, 0, s>>>(sk, sp, nnz, colbits, col_ind, data, row_ptr, err);
   exclusive_scan_u32(row_ptr, row_ptr, a.m, ar);
   uint32_t herr = 0;
   cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s);
@@ -121,14 +126,27 @@ int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar) {
 int build_merge_plan(Format& f, Arena& ar) {
   cudaStream_t s = ar.stream();
   const uint64_t total = (uint64_t)f.m + f.nnz;
-  const uint64_t tiles = (total + kMergeTile - 1) / kMergeTile;
+  int th = kMergeThreads, ipt = kMergeIpt, var = kMergeVariant;
+  if (const char* e = getenv("SPMVLAB_MERGE_CFG")) {  // developer override "threads,ipt,variant"
+    int a = 0, b = 0, c = 0;
+    if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && merge_shape_supported(a, b, c)) {
+      th = a;
+      ipt = b;
+      var = c;
+    }
+  }
+  f.merge_threads = th;
+  f.merge_ipt = ipt;
+  f.merge_variant = var;
+  const uint32_t tile_items = (uint32_t)(th * ipt);
+  const uint64_t tiles = (total + tile_items - 1) / tile_items;
   f.merge_tiles = (uint32_t)tiles;
   uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + 1, 4, s));
   uint32_t* tnnz = static_cast<uint32_t*>(f.add("merge_tile_nnz", tiles + 1, 4, s));
   if (!f.add("merge_carry_row", tiles + 1, 4, s) || !f.add("merge_carry_val", tiles + 1, 8, s) || !trow || !tnnz)
     return kNoMemory;
   merge_partition<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, s>>>(
-      f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, kMergeTile, trow, tnnz);
+      f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, tile_items, trow, tnnz);
   // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32].
   const double mean = f.m ? (double)f.nnz / f.m : 0.0;
   uint32_t g = 2;

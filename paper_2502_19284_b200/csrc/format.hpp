@@ -35,6 +35,7 @@ struct spmvlab_cuda_format {
 
   // ---- merge-path plan (CRS formats), spmv_parallel.hpp:82-86 at tile granularity
   uint32_t merge_tiles = 0;
+  uint32_t merge_threads = 256, merge_ipt = 7, merge_variant = 0;  // tile = threads * ipt items
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;

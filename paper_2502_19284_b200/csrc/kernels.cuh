@@ -10,10 +10,12 @@
 
 namespace spmvcu {
 
-// merge-CSR tile geometry: THREADS x ITEMS merge items per CTA tile.
+// merge-CSR tile geometry (default): THREADS x ITEMS merge items per CTA tile.  An odd item count
+// keeps the per-thread strided shared-memory walk free of bank conflicts.
 constexpr int kMergeThreads = 256;
-constexpr int kMergeIpt = 8;
-constexpr int kMergeTile = kMergeThreads * kMergeIpt;
+constexpr int kMergeIpt = 7;
+constexpr int kMergeVariant = 0;
+bool merge_shape_supported(int threads, int ipt, int variant);
 
 // ---- conversions (COO -> format); each returns a Status
 int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar);

@@ -124,18 +124,21 @@ __global__ void rs_hist_scan(uint32_t* hist) {
   h[threadIdx.x] = s[threadIdx.x];
 }
 
-constexpr size_t kOnesweepSmem =
-    sizeof(uint64_t) * kTile + sizeof(uint32_t) * kTile + sizeof(uint32_t) * kWarps * 256 +
-    sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
+template <typename V>
+constexpr size_t onesweep_smem() {
+  return sizeof(uint64_t) * kTile + sizeof(V) * kTile + sizeof(uint32_t) * kWarps * 256 +
+         sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
+}
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads) rs_onesweep(
-    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
-    uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t dmask,
+    const uint64_t* __restrict__ kin, const V* __restrict__ vin, uint64_t* __restrict__ kout,
+    V* __restrict__ vout, uint64_t n, int shift, uint32_t dmask,
     const uint32_t* __restrict__ pass_offset, uint64_t* status, uint32_t* tile_counter) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kTile);
-  uint32_t* s_whist = s_vals + kTile;          // [warp][digit]
+  V* s_vals = reinterpret_cast<V*>(s_keys + kTile);
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(s_vals + kTile);  // [warp][digit]
   uint32_t* s_local = s_whist + kWarps * 256;  // tile-local exclusive digit offsets
   int64_t* s_gbase = reinterpret_cast<int64_t*>(s_local + 256);
   __shared__ uint32_t s_tile;
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) rs_onesweep(
   const uint64_t wbase = base + (uint64_t)warp * (kIpt * 32);
 
   uint64_t key[kIpt];
-  uint32_t val[kIpt];
+  V val[kIpt];
   uint32_t rank[kIpt];
 #pragma unroll
   for (int i = 0; i < kIpt; ++i) {
@@ -287,7 +290,8 @@ __global__ void __launch_bounds__(kThreads) scan_u32(const uint32_t* in, uint32_
 
 }  // namespace
 
-bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
+template <typename V>
+bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, V* vals, V* vals_alt,
                       uint64_t n, int begin_bit, int end_bit, Arena& arena) {
   if (n <= 1 || end_bit <= begin_bit) return false;
   cudaStream_t s = arena.stream();
@@ -301,9 +305,10 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
   const uint64_t tiles = (n + kTile - 1) / kTile;
   uint64_t* status = arena.alloc_n<uint64_t>(tiles * 256 + 8);
   uint32_t* counter = reinterpret_cast<uint32_t*>(status + tiles * 256);
+  constexpr size_t smem = onesweep_smem<V>();
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOnesweepSmem);
+    cudaFuncSetAttribute(rs_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
   bool in_alt = false;
@@ -312,16 +317,18 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
     const int bits = std::min(8, end_bit - shift);
     cudaMemsetAsync(status, 0, sizeof(uint64_t) * (tiles * 256 + 8), s);
     const uint64_t* ki = in_alt ? keys_alt : keys;
-    const uint32_t* vi = in_alt ? vals_alt : vals;
+    const V* vi = in_alt ? vals_alt : vals;
     uint64_t* ko = in_alt ? keys : keys_alt;
-    uint32_t* vo = in_alt ? vals : vals_alt;
-    rs_onesweep<<<(unsigned)tiles, kThreads, kOnesweepSmem, s>>>(ki, vi, ko, vo, n, shift,
-                                                                (1u << bits) - 1u, hist + p * 256,
-                                                                status, counter);
+    V* vo = in_alt ? vals : vals_alt;
+    rs_onesweep<V><<<(unsigned)tiles, kThreads, smem, s>>>(ki, vi, ko, vo, n, shift, (1u << bits) - 1u,
+                                                           hist + p * 256, status, counter);
     in_alt = !in_alt;
   }
   return in_alt;
 }
+
+template bool radix_sort_pairs<uint32_t>(uint64_t*, uint64_t*, uint32_t*, uint32_t*, uint64_t, int, int, Arena&);
+template bool radix_sort_pairs<uint64_t>(uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t, int, int, Arena&);
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, Arena& arena) {
   cudaStream_t s = arena.stream();

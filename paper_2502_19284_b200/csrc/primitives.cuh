@@ -29,7 +29,9 @@ class Arena {
 
 // Sorts n pairs by key bits [begin_bit, end_bit).  Stable.  Uses keys_alt/vals_alt as ping-pong
 // buffers; returns true if the result ended in the *_alt buffers.
-bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
+// V = uint32_t (an index payload) or uint64_t (a value's bit pattern carried through the sort).
+template <typename V>
+bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, V* vals, V* vals_alt,
                       uint64_t n, int begin_bit, int end_bit, Arena& arena);
 
 // out[0..n] = exclusive prefix sums of in[0..n); out[n] = total.  in and out may alias.
