@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the SpMV hot path (BASELINE.json metric: SpMV GFLOP/s & HBM GB/s per format;
+conversion ms).
+
+Default (N = 1): BASELINE.json configs[1] -- R-MAT scale 22, edge factor 16, (.57,.19,.19,.05),
+duplicates summed, values U(0,1] -- generated on the device from a fixed seed.  One "step" is one
+merge-CSR multiply y = A x (the north-star engine, spmv_merge) through the C ABI with A, x and y
+resident in HBM; `value` = 2 nnz K / t  (GFLOP/s).  Inputs (866 MB of algorithmic bytes) are
+larger than the 126 MB L2, so no flush is needed between steps.
+
+N > 1 (torchrun, one process per GPU): the same matrix is row-sharded by nonzeros across ranks
+(partition_rows_by_nnz with beta = 1, inc/block_size.hpp:73-102); a step is the local multiply
+y_r = A_r x followed by the all-gather of the y_r slices over NCCL (the iterated-SpMV exchange);
+time is the max over ranks; scaling "strong".
+
+Extra keys: e2e (host buffers through the C ABI, copies timed), roofline (dominant kernel,
+event-timed in the library), cpu_baseline (the reference's own engine on the host cores),
+clocks, gpu_launches, formats (every engine: conversion ms, SpMV us, GFLOP/s, GB/s, fraction of
+the measured HBM peak, break-even count).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the unmodified headers)
+timed on the host cores on the same matrix (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "GFLOP/s"
+CONFIG_DESC = {
+    1: "cfg1: Erdos-Renyi n=65,536, Binomial(n,16/n) rows, U[-1,1]",
+    2: "cfg2: R-MAT scale 22, edge factor 16, (.57,.19,.19,.05), duplicates summed, U(0,1]",
+    3: "cfg3: Zipf degrees (k^-2.1 on [1,2^20]), n=2^24, U[-1,1]",
+    4: "cfg4: 5-point Laplacian 4096^2, seeded symmetric permutation",
+    5: "cfg5: R-MAT scale 26, column-normalised",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------ clocks
+CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+class Clocks:
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={CLOCK_FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [s.strip() for s in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ helpers
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg: int, kernel: str):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e = d.get(f"cfg{cfg}:{kernel}")
+    return e.get("dram_bytes_per_launch") if e else None
+
+
+def ev_time(fn, reps: int, warmup: int, stream) -> list:
+    for _ in range(warmup):
+        fn()
+    out = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return out
+
+
+def make_matrix(cfg: int, device):
+    from paper_2502_19284_b200 import gen
+    name, fn = gen.CONFIGS[cfg]
+    m, n, r, c, v = fn(device)
+    return name, m, n, r, c, v
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_reference(m, n, r, c, v, reps: int, warmup: int):
+    """The reference's merge engine (spmv_merge, inc/spmv_parallel.hpp:130-160) and its CRS
+    conversion, unmodified, through oracle/_ref on all host threads."""
+    from oracle.oracle import Oracle, Reference, reference_available
+    rows = r.cpu().numpy().view(np.uint32)
+    cols = c.cpu().numpy().view(np.uint32)
+    vals = v.cpu().numpy()
+    x = np.random.default_rng(7).uniform(0.0, 1.0, n)
+    if reference_available():
+        lib = Reference()
+        threads = lib.hardware_threads()
+        t0 = time.perf_counter()
+        built = lib.build(2, m, n, rows, cols, vals, threads=threads, build_threads=threads, export=False)
+        conv_s = time.perf_counter() - t0
+        mn, tot = lib.time_spmv(built, 2, x, threads, reps, warmup)
+        kind = "reference"
+    else:  # the C restatement (single thread)
+        lib = Oracle()
+        threads = 1
+        t0 = time.perf_counter()
+        built = lib.build(2, m, n, rows, cols, vals)
+        conv_s = time.perf_counter() - t0
+        lib.spmv(built, 2, x, p=1)
+        t1 = time.perf_counter()
+        for _ in range(reps):
+            lib.spmv(built, 2, x, p=1)
+        tot = time.perf_counter() - t1
+        mn = tot / reps
+        kind = "port"
+    nnz = len(vals)
+    return {"value": 2 * nnz * reps / tot / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"full matrix ({nnz} nnz), merge engine p={threads}, {reps} multiplies after {warmup} "
+                      f"warm-up; triplet_to_crs conversion {conv_s:.2f} s",
+            "min_ms": mn * 1e3, "mean_ms": tot / reps * 1e3, "conversion_s": conv_s}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    name, m, n, r, c, v = make_matrix(args.config, dev)
+    nnz = v.numel()
+    steps = max(1, args.steps if args.steps <= 200 else 50)
+    cb = cpu_reference(m, n, r, c, v, steps, max(1, min(args.warmup, 3)))
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": steps, "warmup": max(1, min(args.warmup, 3)), "ms_per_step": cb["mean_ms"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": CONFIG_DESC[args.config], "matrix": name, "n": n,
+                                             "nnz": nnz, "engine": "merge (spmv_merge)"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def all_formats(sp, a, m, n, nnz, x, stream, peak, merge_us, threads=8):
+    out = {}
+    parcrs_us = None
+    for alg in sp.all_algorithms:
+        name = sp.algorithm_name(alg)
+        p = threads
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f = sp.build_format(alg, a, p)
+        e1.record(stream)
+        e1.synchronize()
+        conv_ms = e0.elapsed_time(e1)
+        y = torch.empty(m, dtype=torch.float64, device=x.device)
+        reps = 5 if alg == sp.Algorithm.SeqCrs else 20
+        ts = ev_time(lambda: sp.run_spmv(alg, f, x, y, p=p), reps, 3, stream)
+        us = statistics.median(ts) * 1e3
+        byts = sp.storage_report(f).total() + 8 * n + 8 * m
+        if alg == sp.Algorithm.ParCrs:
+            parcrs_us = us
+        out[name] = {"conversion_ms": conv_ms, "spmv_us": us, "spmv_min_us": min(ts) * 1e3,
+                     "gflops": 2 * nnz / us / 1e3, "gbs": byts / us / 1e3, "frac_of_hbm": byts / us / 1e3 / peak,
+                     "algorithmic_bytes": byts}
+        del f, y
+        torch.cuda.empty_cache()
+    for name, d in out.items():
+        t_fmt = d["spmv_us"]
+        d["break_even_vs_merge"] = (d["conversion_ms"] * 1e3 / (merge_us - t_fmt)) if t_fmt < merge_us else None
+        d["conversion_in_parcrs_spmvs"] = d["conversion_ms"] * 1e3 / parcrs_us if parcrs_us else None
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--no-formats", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import paper_2502_19284_b200 as sp
+    sp.capi.load()
+    L = sp.capi.load()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    peak, peak_kind = measured_peak()
+
+    name, m, n, r, c, v = make_matrix(args.config, dev)
+    nnz_total = v.numel()
+    cuts = [0, m]
+    if world > 1:
+        counts = torch.bincount(r.long(), minlength=m).to(torch.int64)
+        prefix = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+        prefix[1:] = torch.cumsum(counts, 0)
+        cuts = sp.partition_rows_by_nnz(prefix.cpu().numpy().astype(np.uint32), world, 0).tolist()
+        lo, hi = cuts[rank], cuts[rank + 1]
+        sel = (r >= lo) & (r < hi)
+        a = sp.TripletMatrix(hi - lo, n, (r[sel] - lo).to(torch.int32).contiguous(), c[sel].contiguous(),
+                             v[sel].contiguous())
+    else:
+        a = sp.TripletMatrix(m, n, r, c, v)
+    m_loc = a.m
+    x = torch.rand(n, generator=torch.Generator(device=dev).manual_seed(7), device=dev, dtype=torch.float64)
+
+    # conversion (COO -> merge-CSR), event-timed
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fmt = sp.build_format(sp.Algorithm.Merge, a, 1)
+    e1.record(stream)
+    e1.synchronize()
+    conv_ms = e0.elapsed_time(e1)
+    y_full = torch.zeros(m, dtype=torch.float64, device=dev)
+    y_loc = y_full[cuts[rank]:cuts[rank + 1]] if world > 1 else y_full
+
+    def step():
+        sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
+        if world > 1:
+            import torch.distributed as dist
+            works = [dist.broadcast(y_full[cuts[q]:cuts[q + 1]], src=q, async_op=True) for q in range(world)]
+            for w in works:
+                w.wait()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    L.spmvlab_cuda_kernel_timing(1)
+    launches0 = L.spmvlab_cuda_launch_count()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = L.spmvlab_cuda_launch_count() - launches0
+    L.spmvlab_cuda_kernel_timing(0)
+    import ctypes as C
+    kms, kl, kname = C.c_double(), C.c_uint64(), C.create_string_buffer(64)
+    L.spmvlab_cuda_kernel_time(C.byref(kms), C.byref(kl), kname, 64)
+    clk = clocks.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([elapsed_ms, float(launches)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed_ms, launches = float(mx[0]), int(sm[1])
+    ms_step = elapsed_ms / args.steps
+    value = 2.0 * nnz_total * args.steps / (elapsed_ms / 1e3) / 1e9
+
+    # dominant kernel roofline (per launch, this rank)
+    rep = sp.storage_report(fmt)
+    alg_bytes = rep.total() + 8 * n + 8 * m_loc
+    k_ms = kms.value / max(1, kl.value)
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    kernel_name = kname.value.decode()
+    roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": k_ms,
+                "algorithmic_bytes_per_launch": alg_bytes, "traffic": ncu_traffic(args.config, kernel_name),
+                "share_of_step": k_ms / ms_step}
+
+    # end to end through the C ABI with host buffers (H2D x, multiply, D2H y)
+    x_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    x_host.copy_(x.cpu())
+    y_host = torch.empty(m_loc, dtype=torch.float64).pin_memory()
+    x_dev = torch.empty_like(x)
+    y_dev = torch.empty(m_loc, dtype=torch.float64, device=dev)
+    e2e_steps = max(3, min(args.steps, 200))
+
+    def e2e_step():
+        sp.run_spmv_host(sp.Algorithm.Merge, fmt, x_host, y_host, 1, x_dev, y_dev)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    t1.record(stream)
+    t1.synchronize()
+    e2e_ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0])
+    e2e = {"value": 2.0 * nnz_total * e2e_steps / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * m_loc, "ms_per_step": e2e_ms / e2e_steps}
+
+    formats = None
+    merge_us = ms_step * 1e3
+    if world == 1 and not args.no_formats:
+        del y_host, x_host
+        formats = all_formats(sp, a, m, n, nnz_total, x, stream, peak, merge_us)
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_reference(m, n, r, c, v, reps=10, warmup=1)
+            cpu_baseline = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu_baseline["conversion_s"] = cb["conversion_s"]
+        except Exception as ex:  # the checker is optional on a box without oracle/_ref
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                            "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, generated on device)",
+                "config": {"workload": CONFIG_DESC[args.config], "matrix": name, "n": n, "nnz": nnz_total,
+                           "engine": "merge-CSR (spmv_merge)",
+                           "parallelism": f"row-shard x{world} + NCCL all-gather of y" if world > 1 else "1 GPU",
+                           "l2": "inputs larger than L2 (no flush)", "conversion_ms": conv_ms},
+                "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clk,
+                "gpu_launches": launches, "formats": formats}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

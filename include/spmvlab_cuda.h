@@ -134,6 +134,17 @@ int spmvlab_cuda_sort_pairs(uint64_t* keys, uint32_t* values, uint64_t count, in
 /* Exclusive scan: out[0..n] (out[n] = total). */
 int spmvlab_cuda_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, void* stream);
 
+/* --- instrumentation (benchmark harness only) -------------------------------------------------- */
+
+/* Number of CUDA kernels this library has launched since load. */
+uint64_t spmvlab_cuda_launch_count(void);
+
+/* While enabled, the dominant kernel of every multiply is bracketed by CUDA events recorded on
+ * the stream it is launched on.  spmvlab_cuda_kernel_time() waits for those events and returns
+ * the summed kernel duration (ms), the launch count and the kernel's name, then resets. */
+void spmvlab_cuda_kernel_timing(int enable);
+int spmvlab_cuda_kernel_time(double* total_ms, uint64_t* launches, char* name, size_t name_cap);
+
 #ifdef __cplusplus
 }
 #endif

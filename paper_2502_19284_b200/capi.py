@@ -20,6 +20,7 @@ EXPORTS = [
     "spmvlab_cuda_free_format", "spmvlab_cuda_validate", "spmvlab_cuda_select_block_size",
     "spmvlab_cuda_partition_rows_by_nnz", "spmvlab_cuda_merge_path_search",
     "spmvlab_cuda_curve_keys", "spmvlab_cuda_sort_pairs", "spmvlab_cuda_exclusive_scan",
+    "spmvlab_cuda_launch_count", "spmvlab_cuda_kernel_timing", "spmvlab_cuda_kernel_time",
 ]
 
 
@@ -75,5 +76,10 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_curve_keys.argtypes = [i, vp, vp, u64, C.c_uint, vp, vp]
     L.spmvlab_cuda_sort_pairs.argtypes = [vp, vp, u64, i, i, vp]
     L.spmvlab_cuda_exclusive_scan.argtypes = [vp, vp, u64, vp]
+    L.spmvlab_cuda_launch_count.restype = u64
+    L.spmvlab_cuda_launch_count.argtypes = []
+    L.spmvlab_cuda_kernel_timing.restype = None
+    L.spmvlab_cuda_kernel_timing.argtypes = [i]
+    L.spmvlab_cuda_kernel_time.argtypes = [C.POINTER(C.c_double), C.POINTER(u64), C.c_char_p, C.c_size_t]
     _lib = L
     return L

@@ -115,6 +115,8 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   const DevArray* ci = f.find("col_inc");
   const DevArray* rj = f.find("row_jump");
   const DevArray* cs = f.find("chunk_state");
+  note_launch();
+  timing_begin(icrs ? "blocked_spmv_kernel<icrs>" : "blocked_spmv_kernel<packed>", s);
   if (icrs)
     blocked_spmv_kernel<true><<<blocks, 256, 0, s>>>(
         nullptr, ci->as<uint16_t>(), rj->as<uint16_t>(), f.find("data")->as<double>(),
@@ -125,6 +127,7 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
         pk->as<uint32_t>(), nullptr, nullptr, f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
         f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), f.work_items, f.log2_beta, x,
         y);
+  timing_end(s);
   return check_launch("spmv_blocked");
 }
 

@@ -3,9 +3,12 @@
 // Mirrors the reference's algorithm interface (inc/engine.hpp:84-160): engine_block_size,
 // build_format, run_spmv (argument checks of check_spmv_args, inc/spmv_parallel.hpp:90-99, and the
 // BCOH band check, :339-341), storage_report.  Errors become return codes (ErrorKind + 1).
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -63,6 +66,58 @@ int partition_rows_by_nnz_host(const uint32_t* prefix, uint32_t m, unsigned p, u
     prev_cut = cut;
   }
   return kOk;
+}
+
+// ---------------------------------------------------------------- instrumentation
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+struct KernelTimer {
+  std::mutex mu;
+  bool enabled = false;
+  std::vector<cudaEvent_t> ev;  // start/stop pairs
+  size_t used = 0;              // pairs recorded since the last flush
+  double total_ms = 0.0;
+  uint64_t launches = 0;
+  std::string name;
+  static constexpr size_t kPairs = 4096;
+
+  void flush_locked() {
+    for (size_t i = 0; i < used; ++i) {
+      cudaEventSynchronize(ev[2 * i + 1]);
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]) == cudaSuccess) total_ms += ms;
+    }
+    used = 0;
+  }
+};
+KernelTimer& timer() {
+  static KernelTimer t;
+  return t;
+}
+}  // namespace
+
+void timing_begin(const char* kernel, cudaStream_t s) {
+  KernelTimer& t = timer();
+  if (!t.enabled) return;
+  std::lock_guard<std::mutex> lk(t.mu);
+  if (t.ev.empty()) {
+    t.ev.resize(2 * KernelTimer::kPairs);
+    for (auto& e : t.ev) cudaEventCreate(&e);
+  }
+  if (t.used == KernelTimer::kPairs) t.flush_locked();
+  t.name = kernel;
+  cudaEventRecord(t.ev[2 * t.used], s);
+}
+
+void timing_end(cudaStream_t s) {
+  KernelTimer& t = timer();
+  if (!t.enabled) return;
+  std::lock_guard<std::mutex> lk(t.mu);
+  cudaEventRecord(t.ev[2 * t.used + 1], s);
+  ++t.used;
+  ++t.launches;
 }
 
 }  // namespace spmvcu
@@ -323,6 +378,29 @@ int spmvlab_cuda_sort_pairs(uint64_t* keys, uint32_t* values, uint64_t count, in
   }
   ar.release();
   return check_launch("sort_pairs");
+}
+
+uint64_t spmvlab_cuda_launch_count(void) { return g_launches.load(); }
+
+void spmvlab_cuda_kernel_timing(int enable) {
+  KernelTimer& t = timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  t.enabled = enable != 0;
+}
+
+int spmvlab_cuda_kernel_time(double* total_ms, uint64_t* launches, char* name, size_t cap) {
+  KernelTimer& t = timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  t.flush_locked();
+  if (total_ms) *total_ms = t.total_ms;
+  if (launches) *launches = t.launches;
+  if (name && cap) {
+    std::strncpy(name, t.name.c_str(), cap - 1);
+    name[cap - 1] = 0;
+  }
+  t.total_ms = 0.0;
+  t.launches = 0;
+  return kOk;
 }
 
 int spmvlab_cuda_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, void* stream) {

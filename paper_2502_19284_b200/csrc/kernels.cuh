@@ -37,6 +37,11 @@ int curve_keys(int kind, const uint32_t* rows, const uint32_t* cols, uint64_t co
                uint64_t* keys, cudaStream_t s);
 int validate_coo(const spmvlab_cuda_coo& a, Arena& ar);
 
+// ---- instrumentation: launch counter and dominant-kernel event brackets (capi.cu)
+void note_launch(unsigned n = 1);
+void timing_begin(const char* kernel, cudaStream_t s);  // no-op unless enabled
+void timing_end(cudaStream_t s);
+
 inline unsigned grid_for(uint64_t n, unsigned threads, unsigned max_blocks = kNumSMs * 16) {
   uint64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;

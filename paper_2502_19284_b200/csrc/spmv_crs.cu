@@ -350,9 +350,12 @@ void launch_merge_tma(const Format& f, const double* x, double* y, cudaStream_t 
 
 int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.m == 0) return kOk;
+  timing_begin("seq_crs_kernel", s);
   seq_crs_kernel<<<(f.m + 127) / 128, 128, 0, s>>>(f.find("row_ptr")->as<uint32_t>(),
                                                    f.find("col_ind")->as<uint32_t>(),
                                                    f.find("data")->as<double>(), x, y, f.m);
+  timing_end(s);
+  note_launch();
   return check_launch("spmv_seq_crs");
 }
 
@@ -362,6 +365,7 @@ int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   const uint32_t* ci = f.find("col_ind")->as<uint32_t>();
   const double* d = f.find("data")->as<double>();
   const unsigned blocks = grid_for((uint64_t)f.m * f.par_group, 256, kNumSMs * 8);
+  note_launch();
   switch (f.par_group) {
     case 2: par_crs_kernel<2><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
     case 4: par_crs_kernel<4><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
@@ -385,6 +389,7 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.merge_tiles == 0) return kOk;
   const int threads = (int)f.merge_threads, ipt = (int)f.merge_ipt, variant = (int)f.merge_variant;
   bool launched = false;
+  timing_begin(variant == 1 ? "merge_spmv_tma_kernel" : "merge_spmv_kernel", s);
 #define SPMV_MERGE_SHAPE(T, I, V)                                    \
   if (!launched && threads == T && ipt == I && variant == V) {       \
     if (V == 0) launch_merge_direct<T, I, 0>(f, x, y, s);            \
@@ -394,10 +399,12 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   }
 #include "merge_shapes.inc"
 #undef SPMV_MERGE_SHAPE
+  timing_end(s);
   if (!launched) {
     g_last_error = "merge tile shape not instantiated";
     return kInvalidArgument;
   }
+  note_launch(2);
   merge_fixup_kernel<<<(f.merge_tiles + 255) / 256, 256, 0, s>>>(
       f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>(), f.merge_tiles, y, f.m);
   return check_launch("spmv_merge");
