@@ -1,0 +1,18 @@
+"""Runs the C++ drop-in parity program (tests/cpp/dropin_parity.cpp): the reference's call
+pattern (build_format / run_spmv / storage_report on host vectors) through
+include/spmvlab_cuda/engine.hpp and the C ABI, all 11 engines checked against the C oracle."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cpp_dropin_parity(cuda):
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_parity")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.dirname(exe)], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
