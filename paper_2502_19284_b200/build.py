@@ -29,7 +29,7 @@ def sources():
 
 def _deps_mtime():
     return max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC)
-               if f.endswith((".cu", ".cuh", ".hpp"))) if os.path.isdir(CSRC) else 0
+               if f.endswith((".cu", ".cuh", ".hpp", ".inc", ".h"))) if os.path.isdir(CSRC) else 0
 
 
 def _compile(src: str, verbose: bool) -> str:

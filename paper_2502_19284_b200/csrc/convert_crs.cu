@@ -138,7 +138,7 @@ int build_merge_plan(Format& f, Arena& ar) {
   f.merge_threads = th;
   f.merge_ipt = ipt;
   f.merge_variant = var;
-  const uint32_t tile_items = (uint32_t)(th * ipt);
+  const uint32_t tile_items = merge_tile_items(th, ipt, var);
   const uint64_t tiles = (total + tile_items - 1) / tile_items;
   f.merge_tiles = (uint32_t)tiles;
   uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + 1, 4, s));

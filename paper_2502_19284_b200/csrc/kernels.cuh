@@ -10,12 +10,17 @@
 
 namespace spmvcu {
 
-// merge-CSR tile geometry (default): THREADS x ITEMS merge items per CTA tile.  An odd item count
-// keeps the per-thread strided shared-memory walk free of bank conflicts.
-constexpr int kMergeThreads = 256;
+// merge-CSR tile kernels (spmv_crs.cu) and the default shape.  For kVariantShuffle a tile is one
+// warp's 32 * ipt merge items (ipt = groups of 32 nonzeros in flight per lane); for the others a
+// tile is threads * ipt items of one CTA.
+constexpr int kVariantSmem = 0;
+constexpr int kVariantTma = 1;
+constexpr int kVariantShuffle = 2;
+constexpr int kMergeThreads = 128;
 constexpr int kMergeIpt = 7;
-constexpr int kMergeVariant = 0;
+constexpr int kMergeVariant = kVariantSmem;
 bool merge_shape_supported(int threads, int ipt, int variant);
+uint32_t merge_tile_items(int threads, int ipt, int variant);
 
 // ---- conversions (COO -> format); each returns a Status
 int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar);

@@ -6,15 +6,20 @@
 //  * ParCrs (spmv_parcrs, inc/spmv_parallel.hpp:106-125): rows claimed by sub-warp groups whose
 //    width is the next power of two >= the mean row length; lanes stride the row, shuffle-reduce.
 //  * Merge (spmv_merge, inc/spmv_parallel.hpp:130-160): the merge path over (row_ptr[1..m],
-//    0..nnz-1) is cut into equal tiles of THREADS*IPT items at build time (merge_partition, one
-//    diagonal search per tile boundary).  Per tile a CTA stages the row ends and the products
-//    val*x[col] in shared memory (coalesced streaming loads, or TMA bulk copies in the persistent
-//    variant), then every thread merges IPT consecutive path items.  Each thread's starting path
-//    point comes from scattering the row ends to the threads that consume them (no per-thread
-//    binary search), rows that cross threads are combined by a block-wide segmented scan, the y
-//    values of the tile's rows are written with coalesced stores, and the tile leaves one
-//    (row, partial) carry-out.  A fix-up kernel adds the carries of rows spanning tiles in tile
-//    order (deterministic; mirrors the sequential carry loop at spmv_parallel.hpp:157-159).
+//    0..nnz-1) is cut into equal tiles at build time (merge_partition: one diagonal search per
+//    tile boundary, spmv_parallel.hpp:47-86).  Each tile leaves one (row, partial) carry-out and a
+//    fix-up kernel adds the carries of rows spanning tiles in tile order (deterministic; the
+//    sequential carry loop of spmv_parallel.hpp:157-159).  Three tile kernels:
+//      - kVariantSmem (default): one tile of THREADS*IPT items per CTA; coalesced streaming loads
+//        of row ends / col_ind / data (all IPT in flight per thread), IPT x gathers in flight,
+//        products staged in shared memory, per-thread merge walk of IPT items (odd IPT: no bank
+//        conflicts), CTA-wide segmented scan, coalesced y stores.
+//      - kVariantShuffle: one tile per WARP and no shared memory: coalesced 32-element groups,
+//        row-start mask by OR-reduction, shuffle segmented scan, y stored by the row-end lanes.
+//        Measured ~6% slower: warp shuffles occupy the same L1 data pipe as the x gathers.
+//      - kVariantTma: persistent CTAs fed by TMA bulk copies (cp.async.bulk + mbarrier ring).
+//        Measured ~20% slower: fewer resident CTAs leave the x-gather latency exposed.
+//    The floor for all three on R-MAT s22 is the x-gather rate (tools/microbench).
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -60,6 +65,119 @@ __global__ void __launch_bounds__(256) par_crs_kernel(const uint32_t* __restrict
   }
 }
 
+// ---------------------------------------------------------------- shuffle variant (default)
+
+// Consumes every row end (rows rp.. < r1) with end E <= jlim, 32 per batch: the lane holding row r
+// writes y[r] = (sum of the row's products in the group [j, jlim), fetched from the tail lane of
+// its segment, 0 if it has none) + carry for rp0, the row in progress at the group start.
+// Sets `any` if a row end was consumed and `last_end` to the end of the last one.
+__device__ __forceinline__ void consume_row_ends(const uint32_t* __restrict__ row_ptr, double* __restrict__ y,
+                                                 uint32_t& rp, uint32_t r1, uint32_t j, uint32_t jlim,
+                                                 double s, double carry, bool& any, uint32_t& last_end,
+                                                 unsigned lane) {
+  const uint32_t rp0 = rp;
+  uint32_t prev_last = j;  // end of the row preceding the batch (any value <= j for the first batch)
+  while (rp < r1) {
+    const uint32_t r = rp + lane;
+    const bool have = r < r1;
+    const uint32_t E = have ? __ldg(row_ptr + r + 1) : 0xFFFFFFFFu;
+    const bool in = have && E <= jlim;
+    const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
+    uint32_t prevE = __shfl_up_sync(0xFFFFFFFFu, E, 1);
+    if (lane == 0) prevE = prev_last;
+    const bool has = E > max(prevE, j);  // row r owns elements inside this group
+    const int pos = (int)E - 1 - (int)j;  // its tail lane
+    double v = __shfl_sync(0xFFFFFFFFu, s, (in && has) ? pos : 0);
+    if (!has) v = 0.0;
+    if (r == rp0) v += carry;
+    if (in) y[r] = v;
+    const int nin = __popc(inmask);
+    if (nin) {
+      last_end = __shfl_sync(0xFFFFFFFFu, E, nin - 1);
+      prev_last = last_end;
+      any = true;
+      rp += (uint32_t)nin;
+    }
+    if (nin < 32) break;
+  }
+}
+
+template <int U, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) merge_spmv_shfl_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
+    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+    double* __restrict__ carry_val, uint32_t tiles) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t t = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (t >= tiles) return;
+  const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+  const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  uint32_t rp = r0;    // first row whose end has not been consumed by this tile
+  double carry = 0.0;  // this tile's partial sum of row rp
+  for (uint32_t jb = j0; jb < j1; jb += 32 * U) {
+    double p[U];
+    uint32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = jb + 32 * u + lane;
+      const bool ok = k < j1;
+      c[u] = ok ? ld_stream(col + k, pf) : 0u;
+      p[u] = ok ? ld_stream(val + k, pf) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = jb + 32 * u + lane;
+      if (k < j1) p[u] *= ld_x(x + c[u], pl);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = jb + 32 * u;
+      if (j >= j1) break;
+      const uint32_t jend = min(j + 32u, j1);  // group covers elements [j, jend)
+      // row-start mask of the group: a row starting at element j + b sets bit b (bit 0 always)
+      unsigned heads = 1u;
+      {
+        uint32_t q = rp;
+        while (q < r1) {
+          const uint32_t r = q + lane;
+          const uint32_t E = r < r1 ? __ldg(row_ptr + r + 1) : 0xFFFFFFFFu;
+          const bool in = r < r1 && E < jend;
+          heads |= __reduce_or_sync(0xFFFFFFFFu, in && E >= j ? (1u << (E - j)) : 0u);
+          const int nin = __popc(__ballot_sync(0xFFFFFFFFu, r < r1 && E <= jend));
+          q += (uint32_t)nin;
+          if (nin < 32) break;
+        }
+      }
+      // inclusive segmented scan of the products
+      double s = p[u];
+      const int seg = 31 - __clz(heads & (lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u)));
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double o = __shfl_up_sync(0xFFFFFFFFu, s, off);
+        if ((int)lane - off >= seg) s += o;
+      }
+      bool any = false;
+      uint32_t last_end = 0;
+      consume_row_ends(row_ptr, y, rp, r1, j, jend, s, carry, any, last_end, lane);
+      const double s_last = __shfl_sync(0xFFFFFFFFu, s, (int)(jend - 1 - j));
+      if (!any) carry += s_last;                       // the whole group lies inside row rp
+      else carry = (last_end >= jend) ? 0.0 : s_last;  // partial of the row begun in this group
+    }
+  }
+  // rows of this tile ending exactly at j1, and empty rows, after the last nonzero
+  bool any = false;
+  uint32_t last_end = 0;
+  consume_row_ends(row_ptr, y, rp, r1, j1, j1, 0.0, carry, any, last_end, lane);
+  if (lane == 0) {
+    carry_row[t] = r1;
+    carry_val[t] = any ? 0.0 : carry;  // this tile's partial of row r1
+  }
+}
+
+// ---------------------------------------------------------------- shared-memory variant
+
 // Segmented-scan operator on (has_row_end, value): (f1,v1) + (f2,v2) = (f1|f2, f2 ? v2 : v1+v2).
 struct Seg {
   double v;
@@ -76,18 +194,16 @@ struct MergeScratch {
 };
 
 // Merges one staged tile.  srow[0..nrows): row ends row_ptr[r0+1..r1]; sbuf[0..nnzs): products;
-// writes the y values of the tile's rows to sbuf[nnzs .. nnzs+nrows) and returns (in *carry) the
-// tile's partial sum of row r1.  Must be called by all THREADS threads; ends with __syncthreads.
+// writes the y values of the tile's rows to sbuf[nnzs .. nnzs+nrows) and returns the tile's
+// partial sum of row r1.  Called by all THREADS threads; ends with __syncthreads.
 template <int THREADS, int IPT>
 __device__ __forceinline__ double merge_tile(const uint32_t* srow, double* sbuf, int nrows, int nnzs,
                                              uint32_t j0, MergeScratch<THREADS>& sc) {
   constexpr int WARPS = THREADS / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int len = nrows + nnzs;
-
-  // Owner of row end ri = the thread whose IPT-item window holds its path diagonal
-  // ri + (row_end - j0).  Threads learn their starting row as the first row end owned by any
-  // thread >= them (suffix minimum).
+  // Row end ri is consumed at path diagonal ri + (row_end - j0), i.e. by thread diag / IPT; each
+  // thread starts at the first row end owned by a thread >= it (suffix minimum).
   sc.first[tid] = nrows;
   __syncthreads();
   for (int ri = tid; ri < nrows; ri += THREADS) {
@@ -125,8 +241,6 @@ __device__ __forceinline__ double merge_tile(const uint32_t* srow, double* sbuf,
       ++ji;
     }
   }
-
-  // Block-wide inclusive segmented scan of (has_row_end, tail value).
   Seg inc{run, first_row >= 0 ? 1 : 0};
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -154,10 +268,8 @@ __device__ __forceinline__ double merge_tile(const uint32_t* srow, double* sbuf,
   return all.v;
 }
 
-// One tile per CTA; A is staged with coalesced streaming loads (all IPT loads of a thread in
-// flight before any use, then all IPT x gathers).
-template <int THREADS, int IPT, int XMODE>
-__global__ void __launch_bounds__(THREADS, 4) merge_spmv_kernel(
+template <int THREADS, int IPT>
+__global__ void __launch_bounds__(THREADS, 4) merge_spmv_smem_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
@@ -166,13 +278,11 @@ __global__ void __launch_bounds__(THREADS, 4) merge_spmv_kernel(
   __shared__ uint32_t s_rowend[TILE];
   __shared__ double s_buf[TILE];  // [0, nnzs): products; [nnzs, nnzs + nrows): y of the tile's rows
   __shared__ MergeScratch<THREADS> sc;
-
   const int tid = threadIdx.x;
   const uint32_t t = blockIdx.x;
   const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
   const int nrows = (int)(r1 - r0), nnzs = (int)(j1 - j0);
-
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   {
     uint32_t rv[IPT], cv[IPT];
@@ -187,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 4) merge_spmv_kernel(
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const int k = tid + i * THREADS;
-      if (k < nnzs) vv[i] *= ld_xm<XMODE>(x + cv[i], pl);
+      if (k < nnzs) vv[i] *= ld_x(x + cv[i], pl);
     }
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -205,11 +315,8 @@ __global__ void __launch_bounds__(THREADS, 4) merge_spmv_kernel(
   for (int k = tid; k < nrows; k += THREADS) y[r0 + k] = s_buf[nnzs + k];
 }
 
-// Persistent, TMA-pipelined variant.  Each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...;
-// one thread streams the next tiles' col_ind / data / row-end slices into a STAGES-deep ring of
-// shared-memory buffers with 1-D bulk copies (cp.async.bulk, completion on an mbarrier, L2
-// evict-first), so A arrives with no per-thread load instructions while the CTA gathers x and
-// merges the current tile.  Products overwrite the staged values in place.
+// ---------------------------------------------------------------- TMA variant
+
 template <int THREADS, int IPT, int STAGES>
 struct MergeTmaCfg {
   static constexpr int TILE = THREADS * IPT;
@@ -232,7 +339,6 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint4* meta = reinterpret_cast<uint4*>(bars + STAGES);  // (r0, r1, j0, j1) per stage
   __shared__ MergeScratch<THREADS> sc;
-
   const int tid = threadIdx.x;
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
 
@@ -256,13 +362,11 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0)
     for (int s = 0; s < STAGES; ++s) {
       const uint32_t t = blockIdx.x + s * gridDim.x;
       if (t < tiles) issue(t, s);
     }
-  }
-
   int it = 0;
   for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
     const int s = it % STAGES;
@@ -274,7 +378,6 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
     double* sval = reinterpret_cast<double*>(buf + Cfg::VAL_OFF) + (j0 & 3u);
     const uint32_t* scol = reinterpret_cast<const uint32_t*>(buf + Cfg::COL_OFF) + (j0 & 3u);
     const uint32_t* srow = reinterpret_cast<const uint32_t*>(buf + Cfg::ROW_OFF) + ((r0 + 1u) & 3u);
-
     double xv[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -304,26 +407,51 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
   }
 }
 
-// Rows spanning tiles: the head tile of each run of equal carry rows sums the run in tile order.
+// ---------------------------------------------------------------- carry fix-up
+
+// One warp per tile; only run heads do work: the warp sweeps the run 32 carries at a time
+// (coalesced), sums the matching prefix with a fixed shuffle tree, and lane 0 adds the total.
+// Deterministic; O(run / 32) dependent steps even for rows that span hundreds of tiles.
 __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
                                    const double* __restrict__ carry_val, uint32_t tiles,
                                    double* __restrict__ y, uint32_t m) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
   if (t >= tiles) return;
   const uint32_t r = carry_row[t];
-  if (r >= m) return;
-  if (t > 0 && carry_row[t - 1] == r) return;
-  double s = carry_val[t];
-  for (uint32_t u = t + 1; u < tiles && carry_row[u] == r; ++u) s += carry_val[u];
-  y[r] += s;
+  if (r >= m || (t > 0 && carry_row[t - 1] == r)) return;
+  double total = 0.0;
+  for (uint32_t base = t;; base += 32) {
+    const uint32_t u = base + lane;
+    const bool in = u < tiles && carry_row[u] == r;
+    const unsigned match = __ballot_sync(0xFFFFFFFFu, in);
+    const unsigned run = match == 0xFFFFFFFFu ? 32u : (unsigned)(__ffs(~match) - 1);  // matching prefix
+    double v = lane < run ? carry_val[u] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
+    total += v;
+    if (run < 32) break;
+  }
+  if (lane == 0) y[r] += total;
 }
 
-template <int THREADS, int IPT, int XMODE>
-void launch_merge_direct(const Format& f, const double* x, double* y, cudaStream_t s) {
-  merge_spmv_kernel<THREADS, IPT, XMODE><<<f.merge_tiles, THREADS, 0, s>>>(
-      f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(),
-      x, y, f.find("merge_tile_row")->as<uint32_t>(), f.find("merge_tile_nnz")->as<uint32_t>(),
-      f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>());
+// ---------------------------------------------------------------- launchers
+
+#define MERGE_ARGS                                                                                          \
+  f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(), x, y, \
+      f.find("merge_tile_row")->as<uint32_t>(), f.find("merge_tile_nnz")->as<uint32_t>(),                   \
+      f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>()
+
+template <int THREADS, int IPT>
+void launch_merge_shfl(const Format& f, const double* x, double* y, cudaStream_t s) {
+  constexpr int WARPS = THREADS / 32;
+  merge_spmv_shfl_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
+                                                                                             f.merge_tiles);
+}
+
+template <int THREADS, int IPT>
+void launch_merge_smem(const Format& f, const double* x, double* y, cudaStream_t s) {
+  merge_spmv_smem_kernel<THREADS, IPT><<<f.merge_tiles, THREADS, 0, s>>>(MERGE_ARGS);
 }
 
 template <int THREADS, int IPT, int STAGES>
@@ -340,10 +468,7 @@ void launch_merge_tma(const Format& f, const double* x, double* y, cudaStream_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t grid = std::min<uint32_t>(f.merge_tiles, (uint32_t)(sms * grid_per_sm));
-  kern<<<grid, THREADS, Cfg::SMEM, s>>>(
-      f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(),
-      x, y, f.find("merge_tile_row")->as<uint32_t>(), f.find("merge_tile_nnz")->as<uint32_t>(),
-      f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>(), f.merge_tiles);
+  kern<<<grid, THREADS, Cfg::SMEM, s>>>(MERGE_ARGS, f.merge_tiles);
 }
 
 }  // namespace
@@ -376,8 +501,7 @@ int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   return check_launch("spmv_par_crs");
 }
 
-// Tile shapes instantiated for the merge engine: (threads, items per thread, variant).
-// variant 0 = one tile per CTA, direct loads; 1 = persistent TMA-pipelined.
+// Instantiated merge tile shapes (merge_shapes.inc): (threads per CTA, items per thread, variant).
 bool merge_shape_supported(int threads, int ipt, int variant) {
 #define SPMV_MERGE_SHAPE(T, I, V) if (threads == T && ipt == I && variant == V) return true;
 #include "merge_shapes.inc"
@@ -385,16 +509,22 @@ bool merge_shape_supported(int threads, int ipt, int variant) {
   return false;
 }
 
+uint32_t merge_tile_items(int threads, int ipt, int variant) {
+  return (uint32_t)((variant == kVariantShuffle ? 32 : threads) * ipt);
+}
+
 int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.merge_tiles == 0) return kOk;
   const int threads = (int)f.merge_threads, ipt = (int)f.merge_ipt, variant = (int)f.merge_variant;
   bool launched = false;
-  timing_begin(variant == 1 ? "merge_spmv_tma_kernel" : "merge_spmv_kernel", s);
+  timing_begin(variant == kVariantShuffle ? "merge_spmv_shfl_kernel"
+                                          : (variant == kVariantTma ? "merge_spmv_tma_kernel" : "merge_spmv_smem_kernel"),
+               s);
 #define SPMV_MERGE_SHAPE(T, I, V)                                    \
   if (!launched && threads == T && ipt == I && variant == V) {       \
-    if (V == 0) launch_merge_direct<T, I, 0>(f, x, y, s);            \
-    else if (V == 1) launch_merge_tma<T, I, 2>(f, x, y, s);          \
-    else launch_merge_direct<T, I, (V >= 10 ? V - 10 : 0)>(f, x, y, s); \
+    if (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, s);   \
+    else if (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, s); \
+    else launch_merge_tma<T, I, 2>(f, x, y, s);                      \
     launched = true;                                                 \
   }
 #include "merge_shapes.inc"
@@ -405,7 +535,7 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
     return kInvalidArgument;
   }
   note_launch(2);
-  merge_fixup_kernel<<<(f.merge_tiles + 255) / 256, 256, 0, s>>>(
+  merge_fixup_kernel<<<(f.merge_tiles + 7) / 8, 256, 0, s>>>(
       f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>(), f.merge_tiles, y, f.m);
   return check_launch("spmv_merge");
 }
