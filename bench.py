@@ -264,16 +264,12 @@ def main():
 
     name, m, n, r, c, v = make_matrix(args.config, dev)
     nnz_total = v.numel()
+    from paper_2502_19284_b200 import dist as sdist
     cuts = [0, m]
     if world > 1:
-        counts = torch.bincount(r.long(), minlength=m).to(torch.int64)
-        prefix = torch.zeros(m + 1, dtype=torch.int64, device=dev)
-        prefix[1:] = torch.cumsum(counts, 0)
-        cuts = sp.partition_rows_by_nnz(prefix.cpu().numpy().astype(np.uint32), world, 0).tolist()
-        lo, hi = cuts[rank], cuts[rank + 1]
-        sel = (r >= lo) & (r < hi)
-        a = sp.TripletMatrix(hi - lo, n, (r[sel] - lo).to(torch.int32).contiguous(), c[sel].contiguous(),
-                             v[sel].contiguous())
+        cuts = sdist.shard_bounds(sdist.row_prefix(m, r), world)
+        lr, lc, lv = sdist.shard_rows(r, c, v, cuts[rank], cuts[rank + 1])
+        a = sp.TripletMatrix(cuts[rank + 1] - cuts[rank], n, lr, lc, lv)
     else:
         a = sp.TripletMatrix(m, n, r, c, v)
     m_loc = a.m
@@ -289,13 +285,13 @@ def main():
     y_full = torch.zeros(m, dtype=torch.float64, device=dev)
     y_loc = y_full[cuts[rank]:cuts[rank + 1]] if world > 1 else y_full
 
+    sharded = sdist.ShardedSpMV(cuts, rank, lambda xf, yl: sp.run_spmv(sp.Algorithm.Merge, fmt, xf, yl, p=1))
+
     def step():
-        sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
         if world > 1:
-            import torch.distributed as dist
-            works = [dist.broadcast(y_full[cuts[q]:cuts[q + 1]], src=q, async_op=True) for q in range(world)]
-            for w in works:
-                w.wait()
+            sharded.step(x, y_full)  # local merge-CSR multiply + NCCL all-gatherv of the y slices
+        else:
+            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
 
     for _ in range(args.warmup):
         step()
