@@ -339,23 +339,36 @@ def main():
                 "algorithmic_bytes_per_launch": alg_bytes, "traffic": ncu_traffic(args.config, kernel_name),
                 "share_of_step": k_ms / ms_step}
 
-    # end to end through the C ABI with host buffers (H2D x, multiply, D2H y)
-    x_host = torch.empty(n, dtype=torch.float64).pin_memory()
-    x_host.copy_(x.cpu())
-    y_host = torch.empty(m_loc, dtype=torch.float64).pin_memory()
-    x_dev = torch.empty_like(x)
-    y_dev = torch.empty(m_loc, dtype=torch.float64, device=dev)
-    e2e_steps = max(3, min(args.steps, 200))
+    # End to end through the C ABI with host buffers: every step copies its own x in (pinned H2D),
+    # multiplies, and copies its own y out (D2H).  Steps alternate between two streams with their
+    # own staging buffers, so step k+1's H2D overlaps step k's multiply and D2H (full-duplex PCIe).
+    e2e_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    x_host = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    for xh in x_host:
+        xh.copy_(x.cpu())
+    y_host = [torch.empty(m_loc, dtype=torch.float64).pin_memory() for _ in range(2)]
+    x_dev = [torch.empty_like(x) for _ in range(2)]
+    y_dev = [torch.empty(m_loc, dtype=torch.float64, device=dev) for _ in range(2)]
+    e2e_steps = max(4, min(args.steps, 200))
 
-    def e2e_step():
-        sp.run_spmv_host(sp.Algorithm.Merge, fmt, x_host, y_host, 1, x_dev, y_dev)
+    def e2e_run(steps):
+        start = torch.cuda.Event()
+        start.record(stream)
+        for s_ in e2e_streams:
+            s_.wait_event(start)
+        for k in range(steps):
+            i = k & 1
+            sp.run_spmv_host(sp.Algorithm.Merge, fmt, x_host[i], y_host[i], 1, x_dev[i], y_dev[i],
+                             stream=e2e_streams[i])
+        for s_ in e2e_streams:
+            done = torch.cuda.Event()
+            done.record(s_)
+            stream.wait_event(done)
 
-    for _ in range(3):
-        e2e_step()
+    e2e_run(4)
     torch.cuda.synchronize()
     t0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
+    e2e_run(e2e_steps)
     t1.record(stream)
     t1.synchronize()
     e2e_ms = t0.elapsed_time(t1)

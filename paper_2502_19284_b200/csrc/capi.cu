@@ -129,6 +129,24 @@ using namespace spmvcu;
 spmvlab_cuda_format::~spmvlab_cuda_format() {
   for (auto& a : arrays)
     if (a.ptr) cudaFree(a.ptr);
+  for (auto& kv : scratch) {
+    cudaFree(kv.second.carry_row);
+    cudaFree(kv.second.carry_val);
+  }
+}
+
+const spmvlab_cuda_format::Scratch* spmvlab_cuda_format::stream_scratch(cudaStream_t s) const {
+  std::lock_guard<std::mutex> lk(scratch_mu);
+  auto it = scratch.find(s);
+  if (it != scratch.end()) return &it->second;
+  Scratch sc;
+  const uint64_t n = (uint64_t)merge_tiles + 1;
+  if (cudaMalloc(&sc.carry_row, 4 * n) != cudaSuccess || cudaMalloc(&sc.carry_val, 8 * n) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(sc.carry_row);
+    return nullptr;
+  }
+  return &scratch.emplace(s, sc).first->second;
 }
 
 DevArray* spmvlab_cuda_format::find(const std::string& name) {

@@ -143,8 +143,9 @@ int build_merge_plan(Format& f, Arena& ar) {
   f.merge_tiles = (uint32_t)tiles;
   uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + 1, 4, s));
   uint32_t* tnnz = static_cast<uint32_t*>(f.add("merge_tile_nnz", tiles + 1, 4, s));
-  if (!f.add("merge_carry_row", tiles + 1, 4, s) || !f.add("merge_carry_val", tiles + 1, 8, s) || !trow || !tnnz)
-    return kNoMemory;
+  if (!trow || !tnnz) return kNoMemory;
+  // carry scratch is per stream (Format::stream_scratch); pre-create the build stream's
+  if (!f.stream_scratch(s)) return kNoMemory;
   merge_partition<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, s>>>(
       f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, tile_items, trow, tnnz);
   // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32].

@@ -9,6 +9,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,6 +45,16 @@ struct spmvlab_cuda_format {
   // ---- blocked plan (CSB / MergeB / BCOH): work items = (element range, y window)
   uint32_t work_items = 0;
   bool needs_zero_y = false;
+
+  // ---- per-stream multiply scratch (merge carries), so one immutable format can serve
+  // concurrent multiplies on different streams / host threads (inc/engine.hpp ownership rules).
+  struct Scratch {
+    uint32_t* carry_row = nullptr;
+    double* carry_val = nullptr;
+  };
+  mutable std::mutex scratch_mu;
+  mutable std::map<cudaStream_t, Scratch> scratch;
+  const Scratch* stream_scratch(cudaStream_t s) const;  // nullptr on allocation failure
 
   ~spmvlab_cuda_format();
   DevArray* find(const std::string& name);

@@ -439,23 +439,25 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
 
 #define MERGE_ARGS                                                                                          \
   f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(), x, y, \
-      f.find("merge_tile_row")->as<uint32_t>(), f.find("merge_tile_nnz")->as<uint32_t>(),                   \
-      f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>()
+      f.find("merge_tile_row")->as<uint32_t>(), f.find("merge_tile_nnz")->as<uint32_t>(), sc->carry_row,    \
+      sc->carry_val
+
+using Scratch = Format::Scratch;
 
 template <int THREADS, int IPT>
-void launch_merge_shfl(const Format& f, const double* x, double* y, cudaStream_t s) {
+void launch_merge_shfl(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   constexpr int WARPS = THREADS / 32;
   merge_spmv_shfl_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
                                                                                              f.merge_tiles);
 }
 
 template <int THREADS, int IPT>
-void launch_merge_smem(const Format& f, const double* x, double* y, cudaStream_t s) {
+void launch_merge_smem(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   merge_spmv_smem_kernel<THREADS, IPT><<<f.merge_tiles, THREADS, 0, s>>>(MERGE_ARGS);
 }
 
 template <int THREADS, int IPT, int STAGES>
-void launch_merge_tma(const Format& f, const double* x, double* y, cudaStream_t s) {
+void launch_merge_tma(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   using Cfg = MergeTmaCfg<THREADS, IPT, STAGES>;
   auto kern = merge_spmv_tma_kernel<THREADS, IPT, STAGES>;
   static int grid_per_sm = [&] {
@@ -516,16 +518,21 @@ uint32_t merge_tile_items(int threads, int ipt, int variant) {
 int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.merge_tiles == 0) return kOk;
   const int threads = (int)f.merge_threads, ipt = (int)f.merge_ipt, variant = (int)f.merge_variant;
+  const Scratch* sc = f.stream_scratch(s);
+  if (!sc) {
+    g_last_error = "device allocation failed (merge carry scratch)";
+    return kNoMemory;
+  }
   bool launched = false;
   timing_begin(variant == kVariantShuffle ? "merge_spmv_shfl_kernel"
                                           : (variant == kVariantTma ? "merge_spmv_tma_kernel" : "merge_spmv_smem_kernel"),
                s);
 #define SPMV_MERGE_SHAPE(T, I, V)                                    \
   if (!launched && threads == T && ipt == I && variant == V) {       \
-    if (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, s);   \
-    else if (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, s); \
-    else launch_merge_tma<T, I, 2>(f, x, y, s);                      \
-    launched = true;                                                 \
+    if (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);   \
+    else if (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s); \
+    else launch_merge_tma<T, I, 2>(f, x, y, sc, s);                      \
+    launched = true;                                                     \
   }
 #include "merge_shapes.inc"
 #undef SPMV_MERGE_SHAPE
@@ -535,8 +542,7 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
     return kInvalidArgument;
   }
   note_launch(2);
-  merge_fixup_kernel<<<(f.merge_tiles + 7) / 8, 256, 0, s>>>(
-      f.find("merge_carry_row")->as<uint32_t>(), f.find("merge_carry_val")->as<double>(), f.merge_tiles, y, f.m);
+  merge_fixup_kernel<<<(f.merge_tiles + 7) / 8, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m);
   return check_launch("spmv_merge");
 }
 

@@ -167,6 +167,29 @@ def test_radix_sort_and_scan(cuda):
         np.testing.assert_array_equal(out, np.concatenate([[0], np.cumsum(cnt)]))
 
 
+def test_concurrent_streams_share_one_format(cuda, oracle):
+    """Formats are immutable and shareable (inc/engine.hpp ownership): multiplies of
+    one format on several streams at once must not interfere (per-stream carry scratch)."""
+    sp = cuda
+    m, n, r, c, v = random_matrix(20000, 20000, 0.002, seed=21, dense_row_nnz=20000)
+    bound_x = []
+    f = sp.build_format(2, _dev(sp, m, n, r, c, v), 1)
+    ref = oracle.build(0, m, n, r, c, v)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    xs = [np.random.default_rng(100 + i).uniform(-1, 1, n) for i in range(4)]
+    xd = [torch.from_numpy(x).cuda() for x in xs]
+    ys = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in range(4)]
+    torch.cuda.synchronize()
+    for rep in range(5):
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                sp.run_spmv(2, f, xd[i], ys[i], p=1, stream=s)
+    torch.cuda.synchronize()
+    for i in range(4):
+        assert_y_close(ys[i].cpu().numpy(), oracle.spmv(ref, 0, xs[i]), oracle.abs_spmv(m, r, c, v, xs[i]),
+                       what=f"stream {i}")
+
+
 def test_errors(cuda):
     sp = cuda
     m, n, r, c, v = e4()
