@@ -40,6 +40,7 @@ import torch  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "GFLOP/s"
+CPU_MAX_NNZ = 70_000_000  # bound on the CPU-baseline sample (cfg5 has ~1.04G entries)
 CONFIG_DESC = {
     1: "cfg1: Erdos-Renyi n=65,536, Binomial(n,16/n) rows, U[-1,1]",
     2: "cfg2: R-MAT scale 22, edge factor 16, (.57,.19,.19,.05), duplicates summed, U(0,1]",
@@ -145,6 +146,14 @@ def cpu_reference(m, n, r, c, v, reps: int, warmup: int):
     """The reference's merge engine (spmv_merge, inc/spmv_parallel.hpp:130-160) and its CRS
     conversion, unmodified, through oracle/_ref on all host threads."""
     from oracle.oracle import Oracle, Reference, reference_available
+    sample_note = "full matrix"
+    if v.numel() > CPU_MAX_NNZ:  # bound the CPU sample: the leading rows holding <= CPU_MAX_NNZ entries
+        counts = torch.bincount(r.long(), minlength=m)
+        prefix = torch.cumsum(counts, 0)
+        m = int(torch.searchsorted(prefix, torch.tensor([CPU_MAX_NNZ], device=prefix.device)).item())
+        sel = r < m
+        r, c, v = r[sel], c[sel], v[sel]
+        sample_note = f"leading {m} rows"
     rows = r.cpu().numpy().view(np.uint32)
     cols = c.cpu().numpy().view(np.uint32)
     vals = v.cpu().numpy()
@@ -172,7 +181,7 @@ def cpu_reference(m, n, r, c, v, reps: int, warmup: int):
         kind = "port"
     nnz = len(vals)
     return {"value": 2 * nnz * reps / tot / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"full matrix ({nnz} nnz), merge engine p={threads}, {reps} multiplies after {warmup} "
+            "sample": f"{sample_note} ({nnz} nnz), merge engine p={threads}, {reps} multiplies after {warmup} "
                       f"warm-up; triplet_to_crs conversion {conv_s:.2f} s",
             "min_ms": mn * 1e3, "mean_ms": tot / reps * 1e3, "conversion_s": conv_s}
 
@@ -202,13 +211,17 @@ def all_formats(sp, a, m, n, nnz, x, stream, peak, merge_us, threads=8):
     for alg in sp.all_algorithms:
         name = sp.algorithm_name(alg)
         p = threads
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        f = sp.build_format(alg, a, p)
-        e1.record(stream)
-        e1.synchronize()
-        conv_ms = e0.elapsed_time(e1)
+        # conversion time = min of 3 builds (the reference protocol takes the min of its
+        # conversion repetitions, inc/bench.hpp:315-318); the first build also warms the pools
+        conv_ms = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            f = sp.build_format(alg, a, p)
+            e1.record(stream)
+            e1.synchronize()
+            conv_ms = min(conv_ms, e0.elapsed_time(e1))
         y = torch.empty(m, dtype=torch.float64, device=x.device)
         reps = 5 if alg == sp.Algorithm.SeqCrs else 20
         ts = ev_time(lambda: sp.run_spmv(alg, f, x, y, p=p), reps, 3, stream)
@@ -275,13 +288,16 @@ def main():
     m_loc = a.m
     x = torch.rand(n, generator=torch.Generator(device=dev).manual_seed(7), device=dev, dtype=torch.float64)
 
-    # conversion (COO -> merge-CSR), event-timed
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    fmt = sp.build_format(sp.Algorithm.Merge, a, 1)
-    e1.record(stream)
-    e1.synchronize()
-    conv_ms = e0.elapsed_time(e1)
+    # conversion (COO -> merge-CSR), event-timed, min of 2 (the first also warms the memory pools)
+    conv_ms = float("inf")
+    for _ in range(2):
+        fmt = None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fmt = sp.build_format(sp.Algorithm.Merge, a, 1)
+        e1.record(stream)
+        e1.synchronize()
+        conv_ms = min(conv_ms, e0.elapsed_time(e1))
     y_full = torch.zeros(m, dtype=torch.float64, device=dev)
     y_loc = y_full[cuts[rank]:cuts[rank + 1]] if world > 1 else y_full
 

@@ -25,6 +25,19 @@ int check_launch(const char* what) {
 }
 
 void* Arena::alloc(size_t bytes) {
+  static const bool pool_ready = [] {
+    // Keep freed scratch in the device's default stream-ordered pool between builds instead of
+    // returning it to the driver at every synchronisation (conversions allocate GBs of keys).
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    return true;
+  }();
+  (void)pool_ready;
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
   if (cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s_) != cudaSuccess) return nullptr;
