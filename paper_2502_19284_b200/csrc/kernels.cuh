@@ -16,9 +16,10 @@ namespace spmvcu {
 constexpr int kVariantSmem = 0;
 constexpr int kVariantTma = 1;
 constexpr int kVariantShuffle = 2;
-constexpr int kMergeThreads = 128;
+constexpr int kVariantWarpStage = 3;
+constexpr int kMergeThreads = 256;
 constexpr int kMergeIpt = 7;
-constexpr int kMergeVariant = kVariantSmem;
+constexpr int kMergeVariant = kVariantWarpStage;
 bool merge_shape_supported(int threads, int ipt, int variant);
 uint32_t merge_tile_items(int threads, int ipt, int variant);
 

@@ -9,20 +9,26 @@
 //    0..nnz-1) is cut into equal tiles at build time (merge_partition: one diagonal search per
 //    tile boundary, spmv_parallel.hpp:47-86).  Each tile leaves one (row, partial) carry-out and a
 //    fix-up kernel adds the carries of rows spanning tiles in tile order (deterministic; the
-//    sequential carry loop of spmv_parallel.hpp:157-159).  Three tile kernels:
-//      - kVariantSmem (default): one tile of THREADS*IPT items per CTA; coalesced streaming loads
-//        of row ends / col_ind / data (all IPT in flight per thread), IPT x gathers in flight,
-//        products staged in shared memory, per-thread merge walk of IPT items (odd IPT: no bank
-//        conflicts), CTA-wide segmented scan, coalesced y stores.
-//      - kVariantShuffle: one tile per WARP and no shared memory: coalesced 32-element groups,
-//        row-start mask by OR-reduction, shuffle segmented scan, y stored by the row-end lanes.
-//        Measured ~6% slower: warp shuffles occupy the same L1 data pipe as the x gathers.
+//    sequential carry loop of spmv_parallel.hpp:157-159).  Four tile kernels:
+//      - kVariantWarpStage (default, 256 x 7): one tile of 32*IPT items per WARP in warp-private
+//        shared memory, warp synchronisation only: coalesced streaming loads of row ends /
+//        col_ind / data (all IPT in flight per lane), IPT x gathers in flight, products staged,
+//        lane start points by scattering row ends to their owners + shuffle suffix-minimum,
+//        per-lane merge walk of IPT items (odd IPT: bank-conflict free), warp segmented scan,
+//        completed rows stored straight to y.  cfg2: 330 us.
+//      - kVariantSmem: the same with one CTA-wide tile per CTA (CTA barriers).  cfg2: 355 us.
+//      - kVariantShuffle: one tile per warp and no shared memory: coalesced 32-element groups,
+//        row-start mask by OR-reduction, shuffle segmented scan.  cfg2: 388 us (warp shuffles
+//        occupy the same L1 data pipe as the x gathers).
 //      - kVariantTma: persistent CTAs fed by TMA bulk copies (cp.async.bulk + mbarrier ring).
-//        Measured ~20% slower: fewer resident CTAs leave the x-gather latency exposed.
-//    The floor for all three on R-MAT s22 is the x-gather rate (tools/microbench).
+//        cfg2: 427 us (fewer resident CTAs leave the x-gather latency exposed).
+//    The floor for all of them on R-MAT s22 is the x-gather rate (tools/microbench).
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -315,6 +321,114 @@ __global__ void __launch_bounds__(THREADS, 4) merge_spmv_smem_kernel(
   for (int k = tid; k < nrows; k += THREADS) y[r0 + k] = s_buf[nnzs + k];
 }
 
+// ---------------------------------------------------------------- warp-staged variant
+
+// One merge-path tile of 32*IPT items per warp, staged in warp-private shared memory (warp
+// synchronisation only; the warps of an SM drift freely through load / gather / merge phases).
+// Two shared-memory operations per nonzero (striped product store, blocked product load); each
+// lane's starting path point comes from scattering row ends to their owning lanes plus a
+// shuffle suffix-minimum; rows completed by a lane are stored straight to y.
+template <int IPT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 4 ? 48 / WARPS : 12)) merge_spmv_wstage_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
+    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+    double* __restrict__ carry_val, uint32_t tiles) {
+  constexpr int TILE = 32 * IPT;
+  __shared__ uint32_t s_row_all[WARPS][TILE];
+  __shared__ double s_buf_all[WARPS][TILE];
+  __shared__ int s_first_all[WARPS][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x * WARPS + warp;
+  if (t >= tiles) return;
+  uint32_t* srow = s_row_all[warp];
+  double* sbuf = s_buf_all[warp];
+  int* sfirst = s_first_all[warp];
+  const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+  const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
+  const int nrows = (int)(r1 - r0), nnzs = (int)(j1 - j0);
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  {
+    uint32_t rv[IPT], cv[IPT];
+    double vv[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int k = lane + i * 32;
+      rv[i] = k < nrows ? ld_stream(row_ptr + r0 + 1 + k, pf) : 0u;
+      cv[i] = k < nnzs ? ld_stream(col + j0 + k, pf) : 0u;
+      vv[i] = k < nnzs ? ld_stream(val + j0 + k, pf) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int k = lane + i * 32;
+      if (k < nnzs) vv[i] *= ld_x(x + cv[i], pl);
+    }
+    sfirst[lane] = nrows;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int k = lane + i * 32;
+      if (k < nrows) srow[k] = rv[i];
+      if (k < nnzs) sbuf[k] = vv[i];
+    }
+    __syncwarp();
+    // row end k is consumed at path diagonal k + (end - j0): owner lane = diagonal / IPT
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int k = lane + i * 32;
+      if (k < nrows) {
+        const int own = (k + (int)(rv[i] - j0)) / IPT;
+        const int prev = k == 0 ? -1 : (k - 1 + (int)(srow[k - 1] - j0)) / IPT;
+        if (own != prev) sfirst[own] = k;
+      }
+    }
+  }
+  __syncwarp();
+  int mn = sfirst[lane];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_down_sync(0xFFFFFFFFu, mn, off);
+    if (lane + off < 32) mn = min(mn, o);
+  }
+  const int len = nrows + nnzs;
+  const int diag = min(lane * IPT, len);
+  int ri = mn, ji = diag - mn;
+  const int dend = min(diag + IPT, len);
+  double run = 0.0, first_val = 0.0;
+  int first_row = -1;
+  uint32_t next_end = ri < nrows ? srow[ri] : 0xFFFFFFFFu;
+  for (int d = diag; d < dend; ++d) {
+    if (ri < nrows && (ji >= nnzs || next_end <= j0 + (uint32_t)ji)) {
+      if (first_row < 0) { first_row = ri; first_val = run; }
+      else y[r0 + ri] = run;
+      run = 0.0;
+      ++ri;
+      next_end = ri < nrows ? srow[ri] : 0xFFFFFFFFu;
+    } else {
+      run += sbuf[ji];
+      ++ji;
+    }
+  }
+  // warp segmented scan of (has_row_end, tail)
+  double v = run;
+  int fl = first_row >= 0 ? 1 : 0;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ov = __shfl_up_sync(0xFFFFFFFFu, v, off);
+    const int of = __shfl_up_sync(0xFFFFFFFFu, fl, off);
+    if (lane >= off) {
+      if (!fl) v += ov;
+      fl |= of;
+    }
+  }
+  double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+  if (lane == 0) ex = 0.0;
+  if (first_row >= 0) y[r0 + first_row] = first_val + ex;
+  if (lane == 31) {
+    carry_row[t] = r1;
+    carry_val[t] = v;
+  }
+}
+
 // ---------------------------------------------------------------- TMA variant
 
 template <int THREADS, int IPT, int STAGES>
@@ -409,30 +523,50 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
 
 // ---------------------------------------------------------------- carry fix-up
 
-// One warp per tile; only run heads do work: the warp sweeps the run 32 carries at a time
-// (coalesced), sums the matching prefix with a fixed shuffle tree, and lane 0 adds the total.
-// Deterministic; O(run / 32) dependent steps even for rows that span hundreds of tiles.
+// One lane per tile, 32 tiles per warp.  Runs of equal carry rows are summed with a warp segmented
+// scan; the tail lane of a run that starts and ends inside the chunk adds it to y.  A run that
+// starts in the chunk and continues past it is finished by the whole warp sweeping the following
+// carries 32 at a time.  Runs that started in an earlier chunk are left to that chunk's warp.
+// Deterministic (fixed reduction order) and O(run / 32) dependent steps for the longest rows.
 __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
                                    const double* __restrict__ carry_val, uint32_t tiles,
                                    double* __restrict__ y, uint32_t m) {
-  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31u;
-  if (t >= tiles) return;
-  const uint32_t r = carry_row[t];
-  if (r >= m || (t > 0 && carry_row[t - 1] == r)) return;
-  double total = 0.0;
-  for (uint32_t base = t;; base += 32) {
-    const uint32_t u = base + lane;
-    const bool in = u < tiles && carry_row[u] == r;
-    const unsigned match = __ballot_sync(0xFFFFFFFFu, in);
-    const unsigned run = match == 0xFFFFFFFFu ? 32u : (unsigned)(__ffs(~match) - 1);  // matching prefix
-    double v = lane < run ? carry_val[u] : 0.0;
+  const uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
+  if (base >= tiles) return;
+  const uint32_t t = base + lane;
+  const uint32_t r = t < tiles ? carry_row[t] : 0xFFFFFFFFu;
+  double v = t < tiles ? carry_val[t] : 0.0;
+  uint32_t prow = __shfl_up_sync(0xFFFFFFFFu, r, 1);
+  if (lane == 0) prow = base > 0 ? carry_row[base - 1] : ~r;
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, r != prow);
+  const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int seg = 31 - __clz((heads | 1u) & le);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
-    total += v;
-    if (run < 32) break;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double o = __shfl_up_sync(0xFFFFFFFFu, v, off);
+    if ((int)lane - off >= seg) v += o;
   }
-  if (lane == 0) y[r] += total;
+  const bool started_here = (heads >> seg) & 1u;
+  const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+  if (tail && lane != 31 && started_here && r < m) y[r] += v;
+  // the chunk's last run: finish it here if it started here
+  const uint32_t r31 = __shfl_sync(0xFFFFFFFFu, r, 31);
+  const bool own31 = __shfl_sync(0xFFFFFFFFu, started_here, 31);
+  if (!own31 || r31 >= m) return;
+  double total = __shfl_sync(0xFFFFFFFFu, v, 31);
+  for (uint32_t nb = base + 32; nb < tiles; nb += 32) {
+    const uint32_t u = nb + lane;
+    const bool in = u < tiles && carry_row[u] == r31;
+    const unsigned match = __ballot_sync(0xFFFFFFFFu, in);
+    const unsigned runlen = match == 0xFFFFFFFFu ? 32u : (unsigned)(__ffs(~match) - 1);
+    double w = lane < runlen ? carry_val[u] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, off);
+    total += w;
+    if (runlen < 32) break;
+  }
+  if (lane == 0) y[r31] += total;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -449,6 +583,13 @@ void launch_merge_shfl(const Format& f, const double* x, double* y, const Scratc
   constexpr int WARPS = THREADS / 32;
   merge_spmv_shfl_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
                                                                                              f.merge_tiles);
+}
+
+template <int THREADS, int IPT>
+void launch_merge_wstage(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
+  constexpr int WARPS = THREADS / 32;
+  merge_spmv_wstage_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
+                                                                                               f.merge_tiles);
 }
 
 template <int THREADS, int IPT>
@@ -512,7 +653,17 @@ bool merge_shape_supported(int threads, int ipt, int variant) {
 }
 
 uint32_t merge_tile_items(int threads, int ipt, int variant) {
-  return (uint32_t)((variant == kVariantShuffle ? 32 : threads) * ipt);
+  const bool per_warp = variant == kVariantShuffle || variant == kVariantWarpStage;
+  return (uint32_t)((per_warp ? 32 : threads) * ipt);
+}
+
+static const char* merge_kernel_name(int variant) {
+  switch (variant) {
+    case kVariantShuffle: return "merge_spmv_shfl_kernel";
+    case kVariantWarpStage: return "merge_spmv_wstage_kernel";
+    case kVariantTma: return "merge_spmv_tma_kernel";
+    default: return "merge_spmv_smem_kernel";
+  }
 }
 
 int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
@@ -524,12 +675,11 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
     return kNoMemory;
   }
   bool launched = false;
-  timing_begin(variant == kVariantShuffle ? "merge_spmv_shfl_kernel"
-                                          : (variant == kVariantTma ? "merge_spmv_tma_kernel" : "merge_spmv_smem_kernel"),
-               s);
+  timing_begin(merge_kernel_name(variant), s);
 #define SPMV_MERGE_SHAPE(T, I, V)                                    \
   if (!launched && threads == T && ipt == I && variant == V) {       \
     if (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);   \
+    else if (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s); \
     else if (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s); \
     else launch_merge_tma<T, I, 2>(f, x, y, sc, s);                      \
     launched = true;                                                     \
@@ -542,7 +692,7 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
     return kInvalidArgument;
   }
   note_launch(2);
-  merge_fixup_kernel<<<(f.merge_tiles + 7) / 8, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m);
+  merge_fixup_kernel<<<(f.merge_tiles + 255) / 256, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m);
   return check_launch("spmv_merge");
 }
 
