@@ -356,16 +356,18 @@ def main():
                 "share_of_step": k_ms / ms_step}
 
     # End to end through the C ABI with host buffers: every step copies its own x in (pinned H2D),
-    # multiplies, and copies its own y out (D2H).  Steps alternate between two streams with their
-    # own staging buffers, so step k+1's H2D overlaps step k's multiply and D2H (full-duplex PCIe).
-    e2e_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    x_host = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    # multiplies, and copies its own y out (D2H).  Steps rotate over three streams with their own
+    # staging buffers, so the H2D of later steps overlaps the multiply and D2H of earlier ones
+    # (full-duplex PCIe) without waiting behind a stream's own D2H.
+    NS = 3
+    e2e_streams = [torch.cuda.Stream(dev) for _ in range(NS)]
+    x_host = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(NS)]
     for xh in x_host:
         xh.copy_(x.cpu())
-    y_host = [torch.empty(m_loc, dtype=torch.float64).pin_memory() for _ in range(2)]
-    x_dev = [torch.empty_like(x) for _ in range(2)]
-    y_dev = [torch.empty(m_loc, dtype=torch.float64, device=dev) for _ in range(2)]
-    e2e_steps = max(4, min(args.steps, 200))
+    y_host = [torch.empty(m_loc, dtype=torch.float64).pin_memory() for _ in range(NS)]
+    x_dev = [torch.empty_like(x) for _ in range(NS)]
+    y_dev = [torch.empty(m_loc, dtype=torch.float64, device=dev) for _ in range(NS)]
+    e2e_steps = max(6, min(args.steps, 200))
 
     def e2e_run(steps):
         start = torch.cuda.Event()
@@ -373,7 +375,7 @@ def main():
         for s_ in e2e_streams:
             s_.wait_event(start)
         for k in range(steps):
-            i = k & 1
+            i = k % NS
             sp.run_spmv_host(sp.Algorithm.Merge, fmt, x_host[i], y_host[i], 1, x_dev[i], y_dev[i],
                              stream=e2e_streams[i])
         for s_ in e2e_streams:

@@ -107,6 +107,28 @@ void spmvlab_cuda_free_format(spmvlab_cuda_format* f);
 /* validate(const TripletMatrix&) -- inc/triplet.hpp:42-59 (range + duplicate check on device). */
 int spmvlab_cuda_validate(const spmvlab_cuda_coo* a, void* stream);
 
+/* --- SPMVLAB1 binary triplet cache (inc/cache_io.hpp:31-91, inc/io.hpp:29-40) ----------------- */
+
+/* cache_read: tag "SPMVLAB1", m, n, nnz as u64 LE, then nnz u64 row indices, nnz u64 column
+ * indices and nnz u64 value bit patterns.  The file is read in large chunks into pinned staging
+ * buffers while earlier chunks are copied to the device and narrowed there (indices are cast to
+ * the 32-bit index type as the reference does), then the triplet is validated on the device
+ * (inc/triplet.hpp:42-59).  If a->row_ind / col_ind / data are non-NULL they are caller-owned
+ * device buffers of capacity a->nnz entries (size them with spmvlab_cuda_cache_info); otherwise
+ * the library allocates them and they must be released with spmvlab_cuda_free_coo().  Errors:
+ * BadMagic, Truncated, Overflow, IndexOutOfRange, DuplicateEntry, IoError, InvalidArgument (buffer
+ * too small). */
+int spmvlab_cuda_cache_read(const char* path, spmvlab_cuda_coo* a, void* stream);
+
+/* Header of a cache file: m, n, nnz (checks the tag and the dimension limits). */
+int spmvlab_cuda_cache_info(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz);
+
+/* cache_write (inc/cache_io.hpp:58-66) of a device triplet; byte-identical to the reference's. */
+int spmvlab_cuda_cache_write(const char* path, const spmvlab_cuda_coo* a, void* stream);
+
+/* Releases the arrays of a triplet returned by spmvlab_cuda_cache_read. */
+void spmvlab_cuda_free_coo(spmvlab_cuda_coo* a);
+
 /* --- primitives, exposed for parity tests ---------------------------------------------------- */
 
 /* select_block_size -- inc/block_size.hpp:47-61 (value_size 8). Host computation. */

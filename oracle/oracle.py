@@ -130,6 +130,12 @@ class Oracle:
         L.orc_validate.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                    C.POINTER(C.c_uint32)]
         L.orc_verification_input.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_double)]
+        L.orc_cache_read.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_uint64), C.POINTER(C.POINTER(C.c_uint32)),
+                                     C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_double))]
+        L.orc_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+        L.orc_free.argtypes = [C.c_void_p]
 
     # -- formats ----------------------------------------------------------------------------
     def build(self, alg: int, m: int, n: int, rows, cols, vals, threads: int = 1,
@@ -248,6 +254,32 @@ class Oracle:
         self.lib.orc_verification_input(n, seed, _p(x, C.c_double))
         return x
 
+    def cache_read(self, path):
+        """(m, n, rows, cols, vals) or CheckerError (inc/cache_io.hpp:69-91)."""
+        return _cache_read(self.lib.orc_cache_read, self.lib.orc_free, path)
+
+    def cache_write(self, path, m, n, rows, cols, vals):
+        rows, cols, vals = _coo_args(rows, cols, vals)
+        rc = self.lib.orc_cache_write(path.encode(), m, n, len(vals), _p(rows, C.c_uint32),
+                                      _p(cols, C.c_uint32), _p(vals, C.c_double))
+        if rc:
+            raise CheckerError(rc, "orc_cache_write")
+
+
+def _cache_read(fn, free, path):
+    m, n, nnz = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    r, c, v = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_double)()
+    rc = fn(path.encode(), C.byref(m), C.byref(n), C.byref(nnz), C.byref(r), C.byref(c), C.byref(v))
+    if rc:
+        raise CheckerError(rc, f"cache_read {path}")
+    k = nnz.value
+    out = (m.value, n.value, np.ctypeslib.as_array(r, (k,)).copy() if k else np.zeros(0, np.uint32),
+           np.ctypeslib.as_array(c, (k,)).copy() if k else np.zeros(0, np.uint32),
+           np.ctypeslib.as_array(v, (k,)).copy() if k else np.zeros(0))
+    for p in (r, c, v):
+        free(C.cast(p, C.c_void_p))
+    return out
+
 
 class Reference:
     """The unmodified reference (oracle/_ref/libspmvref.so)."""
@@ -284,6 +316,22 @@ class Reference:
                                                 C.POINTER(C.c_uint32)]
         L.ref_verification_input.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_double)]
         L.ref_hardware_threads.restype = C.c_uint
+        L.ref_cache_read.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_uint64), C.POINTER(C.POINTER(C.c_uint32)),
+                                     C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_double))]
+        L.ref_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+        L.ref_free_buf.argtypes = [C.c_void_p]
+
+    def cache_read(self, path):
+        return _cache_read(self.lib.ref_cache_read, self.lib.ref_free_buf, path)
+
+    def cache_write(self, path, m, n, rows, cols, vals):
+        rows, cols, vals = _coo_args(rows, cols, vals)
+        rc = self.lib.ref_cache_write(path.encode(), m, n, len(vals), _p(rows, C.c_uint32),
+                                      _p(cols, C.c_uint32), _p(vals, C.c_double))
+        if rc:
+            self._err(rc, "ref_cache_write")
 
     def _err(self, rc, what):
         raise CheckerError(rc, f"{what}: {self.lib.ref_last_error().decode()}")

@@ -15,8 +15,11 @@
 #include <vector>
 
 #include "spmv_oracle.h"
+#include <fstream>
+
 #include "spmvlab/bench.hpp"
 #include "spmvlab/engine.hpp"
+#include "spmvlab/io.hpp"
 
 using namespace spmvlab;
 
@@ -194,6 +197,44 @@ void ref_free_export(orc_format* f) {
 uint64_t ref_storage_total(void* hv) {
   return storage_report(static_cast<Handle*>(hv)->fmt).total();
 }
+
+// --- SPMVLAB1 cache (inc/cache_io.hpp:58-91) --------------------------------------------------
+int ref_cache_write(const char* path, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows,
+                    const uint32_t* cols, const double* vals) {
+  try {
+    auto a = make_triplet(m, n, nnz, rows, cols, vals);
+    save_cache(a, path);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// Reads a cache; on success *nnz_out and the malloc'ed arrays are returned (free with ref_free_buf).
+int ref_cache_read(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz_out, uint32_t** rows,
+                   uint32_t** cols, double** vals) {
+  try {
+    std::ifstream in(path, std::ios::binary);
+    require(in.is_open(), ErrorKind::IoError, std::string("cannot open ") + path);
+    TripletMatrix a = cache_read(in);
+    *m = a.m;
+    *n = a.n;
+    *nnz_out = a.data.size();
+    *rows = static_cast<uint32_t*>(std::malloc(4 * (a.data.size() + 1)));
+    *cols = static_cast<uint32_t*>(std::malloc(4 * (a.data.size() + 1)));
+    *vals = static_cast<double*>(std::malloc(8 * (a.data.size() + 1)));
+    std::memcpy(*rows, a.row_ind.data(), 4 * a.data.size());
+    std::memcpy(*cols, a.col_ind.data(), 4 * a.data.size());
+    std::memcpy(*vals, a.data.data(), 8 * a.data.size());
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+void ref_free_buf(void* p) { std::free(p); }
 
 // --- primitives (for golden vectors) ---------------------------------------------------------
 unsigned ref_select_block_size(uint64_t n, unsigned cap, uint64_t l2) {

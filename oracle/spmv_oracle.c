@@ -15,6 +15,7 @@
  */
 #include "spmv_oracle.h"
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -240,6 +241,80 @@ void orc_verification_input(uint32_t n, uint64_t seed, double* x) {
     state = state * UINT64_C(6364136223846793005) + UINT64_C(1442695040888963407);
     x[i] = 0.5 + (double)(state >> 11) * 0x1.0p-53;
   }
+}
+
+/* ---------------------------------------------------------------- SPMVLAB1 cache (cache_io.hpp) */
+
+static int get_u64_le(FILE* f, uint64_t* v) { /* cache_io.hpp:47-54 */
+  unsigned char b[8];
+  if (fread(b, 1, 8, f) != 8) return ORC_TRUNCATED;
+  uint64_t x = 0;
+  for (int i = 0; i < 8; ++i) x |= (uint64_t)b[i] << (8 * i);
+  *v = x;
+  return ORC_OK;
+}
+
+static void put_u64_le(FILE* f, uint64_t v) { /* cache_io.hpp:41-45 */
+  unsigned char b[8];
+  for (int i = 0; i < 8; ++i) b[i] = (unsigned char)(v >> (8 * i));
+  fwrite(b, 1, 8, f);
+}
+
+void orc_free(void* p) { free(p); }
+
+/* cache_read, cache_io.hpp:69-91: magic, m, n, nnz, then the three streams; validate(). */
+int orc_cache_read(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz, uint32_t** rows,
+                   uint32_t** cols, double** vals) {
+  static const char magic[8] = {'S', 'P', 'M', 'V', 'L', 'A', 'B', '1'};
+  *rows = NULL;
+  *cols = NULL;
+  *vals = NULL;
+  FILE* f = fopen(path, "rb");
+  if (!f) return ORC_IO_ERROR;
+  char head[8];
+  if (fread(head, 1, 8, f) != 8 || memcmp(head, magic, 8) != 0) { fclose(f); return ORC_BAD_MAGIC; }
+  uint64_t mm, nn, cnt;
+  if (get_u64_le(f, &mm) || get_u64_le(f, &nn) || get_u64_le(f, &cnt)) { fclose(f); return ORC_TRUNCATED; }
+  if (mm > MAX_DIMENSION || nn > MAX_DIMENSION) { fclose(f); return ORC_OVERFLOW; }
+  uint32_t* r = (uint32_t*)malloc(4 * (cnt ? cnt : 1));
+  uint32_t* c = (uint32_t*)malloc(4 * (cnt ? cnt : 1));
+  double* v = (double*)malloc(8 * (cnt ? cnt : 1));
+  int rc = ORC_OK;
+  uint64_t x;
+  for (uint64_t k = 0; k < cnt && !rc; ++k) { rc = get_u64_le(f, &x); r[k] = (uint32_t)x; }
+  for (uint64_t k = 0; k < cnt && !rc; ++k) { rc = get_u64_le(f, &x); c[k] = (uint32_t)x; }
+  for (uint64_t k = 0; k < cnt && !rc; ++k) { rc = get_u64_le(f, &x); memcpy(&v[k], &x, 8); }
+  fclose(f);
+  if (!rc) rc = orc_validate((uint32_t)mm, (uint32_t)nn, cnt, r, c);
+  if (rc) { free(r); free(c); free(v); return rc; }
+  *m = (uint32_t)mm;
+  *n = (uint32_t)nn;
+  *nnz = cnt;
+  *rows = r;
+  *cols = c;
+  *vals = v;
+  return ORC_OK;
+}
+
+/* cache_write, cache_io.hpp:58-66 */
+int orc_cache_write(const char* path, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows,
+                    const uint32_t* cols, const double* vals) {
+  FILE* f = fopen(path, "wb");
+  if (!f) return ORC_IO_ERROR;
+  fwrite("SPMVLAB1", 1, 8, f);
+  put_u64_le(f, m);
+  put_u64_le(f, n);
+  put_u64_le(f, nnz);
+  for (uint64_t k = 0; k < nnz; ++k) put_u64_le(f, rows[k]);
+  for (uint64_t k = 0; k < nnz; ++k) put_u64_le(f, cols[k]);
+  for (uint64_t k = 0; k < nnz; ++k) {
+    uint64_t b;
+    memcpy(&b, &vals[k], 8);
+    put_u64_le(f, b);
+  }
+  const int bad = ferror(f);
+  fclose(f);
+  return bad ? ORC_IO_ERROR : ORC_OK;
 }
 
 /* ---------------------------------------------------------------- key sort helper */

@@ -21,6 +21,7 @@ EXPORTS = [
     "spmvlab_cuda_partition_rows_by_nnz", "spmvlab_cuda_merge_path_search",
     "spmvlab_cuda_curve_keys", "spmvlab_cuda_sort_pairs", "spmvlab_cuda_exclusive_scan",
     "spmvlab_cuda_launch_count", "spmvlab_cuda_kernel_timing", "spmvlab_cuda_kernel_time",
+    "spmvlab_cuda_cache_read", "spmvlab_cuda_cache_write", "spmvlab_cuda_free_coo", "spmvlab_cuda_cache_info",
 ]
 
 
@@ -81,5 +82,10 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_kernel_timing.restype = None
     L.spmvlab_cuda_kernel_timing.argtypes = [i]
     L.spmvlab_cuda_kernel_time.argtypes = [C.POINTER(C.c_double), C.POINTER(u64), C.c_char_p, C.c_size_t]
+    L.spmvlab_cuda_cache_read.argtypes = [C.c_char_p, C.POINTER(Coo), vp]
+    L.spmvlab_cuda_cache_write.argtypes = [C.c_char_p, C.POINTER(Coo), vp]
+    L.spmvlab_cuda_free_coo.argtypes = [C.POINTER(Coo)]
+    L.spmvlab_cuda_free_coo.restype = None
+    L.spmvlab_cuda_cache_info.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]
     _lib = L
     return L

@@ -398,6 +398,30 @@ int spmvlab_cuda_sort_pairs(uint64_t* keys, uint32_t* values, uint64_t count, in
   return check_launch("sort_pairs");
 }
 
+int spmvlab_cuda_cache_read(const char* path, spmvlab_cuda_coo* a, void* stream) {
+  if (!path || !a) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return cache_read(path, a, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_cache_info(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz) {
+  if (!path || !m || !n || !nnz) return fail(kInvalidArgument, "null argument");
+  return cache_info(path, m, n, nnz);
+}
+
+int spmvlab_cuda_cache_write(const char* path, const spmvlab_cuda_coo* a, void* stream) {
+  if (!path || !a) return fail(kInvalidArgument, "null argument");
+  return cache_write(path, *a, static_cast<cudaStream_t>(stream));
+}
+
+void spmvlab_cuda_free_coo(spmvlab_cuda_coo* a) {
+  if (!a) return;
+  cudaFree(const_cast<uint32_t*>(a->row_ind));
+  cudaFree(const_cast<uint32_t*>(a->col_ind));
+  cudaFree(const_cast<double*>(a->data));
+  std::memset(a, 0, sizeof(*a));
+}
+
 uint64_t spmvlab_cuda_launch_count(void) { return g_launches.load(); }
 
 void spmvlab_cuda_kernel_timing(int enable) {

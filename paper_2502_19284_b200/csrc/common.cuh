@@ -16,6 +16,9 @@ enum Status : int {
   kOverflow = 4,
   kIndexOutOfRange = 9,
   kDuplicateEntry = 10,
+  kTruncated = 12,
+  kBadMagic = 13,
+  kIoError = 14,
   kCudaError = 100,
   kNoMemory = 101,
 };

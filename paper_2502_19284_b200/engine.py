@@ -267,6 +267,27 @@ def validate(a: TripletMatrix, stream=None) -> None:
     _check(capi.load().spmvlab_cuda_validate(C.byref(coo), _stream(stream)))
 
 
+def cache_read(path: str, stream=None) -> TripletMatrix:
+    """SPMVLAB1 triplet cache -> device triplet (inc/cache_io.hpp:69-91, validated)."""
+    L = capi.load()
+    m, n, nnz = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _check(L.spmvlab_cuda_cache_info(str(path).encode(), C.byref(m), C.byref(n), C.byref(nnz)))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    k = int(nnz.value)
+    rows = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    cols = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+    coo = capi.Coo(m.value, n.value, k, rows.data_ptr(), cols.data_ptr(), vals.data_ptr())
+    _check(L.spmvlab_cuda_cache_read(str(path).encode(), C.byref(coo), _stream(stream)))
+    return TripletMatrix(int(coo.m), int(coo.n), rows[:k], cols[:k], vals[:k])
+
+
+def cache_write(path: str, a: TripletMatrix, stream=None) -> None:
+    """Device triplet -> SPMVLAB1 cache, byte-identical to the reference's cache_write."""
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_cache_write(str(path).encode(), C.byref(coo), _stream(stream)))
+
+
 def select_block_size(n: int, index_bits_cap: int, l2_bytes: int = DEFAULT_L2_BYTES) -> int:
     """inc/block_size.hpp:47-61 -> log2(beta)."""
     return int(capi.load().spmvlab_cuda_select_block_size(n, index_bits_cap, l2_bytes))
