@@ -93,6 +93,25 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, ui
   return excl;
 }
 
+// Look-back for a tile that has ALREADY published its aggregate (flag AGG, or PREFIX for tile 0):
+// walks predecessors until an inclusive prefix, then publishes its own inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_published(uint64_t* status, uint32_t tile, uint32_t slot,
+                                                       uint32_t slots, uint64_t count) {
+  if (tile == 0) return 0;
+  uint64_t excl = 0;
+  int64_t t = (int64_t)tile - 1;
+  while (true) {
+    const uint64_t v = ld_relaxed(status + (uint64_t)t * slots + slot);
+    const uint64_t flag = v & ~kValMask;
+    if (flag == 0) continue;
+    excl += v & kValMask;
+    if (flag == kFlagPrefix) break;
+    --t;
+  }
+  st_relaxed(status + (uint64_t)tile * slots + slot, kFlagPrefix | (excl + count));
+  return excl;
+}
+
 // ------------------------------------------------------------------ radix sort
 
 __global__ void __launch_bounds__(kThreads) rs_histogram(const uint64_t* __restrict__ keys, uint64_t n,
@@ -137,17 +156,23 @@ __global__ void rs_hist_scan(uint32_t* hist) {
   h[threadIdx.x] = s[threadIdx.x];
 }
 
+// Pairs per thread: 16 with a 32-bit payload; 9 with a 64-bit payload keeps the kernel under ~80
+// registers (3 CTAs / 24 warps per SM instead of 1 CTA at 141 registers).
 template <typename V>
-constexpr size_t onesweep_smem() {
-  return sizeof(uint64_t) * kTile + sizeof(V) * kTile + sizeof(uint32_t) * kWarps * 256 +
-         sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
-}
+struct OneSweep {
+  static constexpr int IPT = sizeof(V) == 8 ? 9 : 16;
+  static constexpr int TILE = kThreads * IPT;
+  static constexpr size_t SMEM = sizeof(uint64_t) * TILE + sizeof(V) * TILE + sizeof(uint32_t) * kWarps * 256 +
+                                 sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
+};
 
 template <typename V>
 __global__ void __launch_bounds__(kThreads) rs_onesweep(
     const uint64_t* __restrict__ kin, const V* __restrict__ vin, uint64_t* __restrict__ kout,
     V* __restrict__ vout, uint64_t n, int shift, uint32_t dmask,
     const uint32_t* __restrict__ pass_offset, uint64_t* status, uint32_t* tile_counter) {
+  constexpr int kIpt = OneSweep<V>::IPT;
+  constexpr int kTile = OneSweep<V>::TILE;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
   V* s_vals = reinterpret_cast<V*>(s_keys + kTile);
@@ -215,21 +240,28 @@ __global__ void __launch_bounds__(kThreads) rs_onesweep(
   uint32_t wpre = 0;
   for (unsigned w = 0; w < warp; ++w) wpre += s_wsum[w];
   const uint32_t local_excl = wpre + incl - cnt;
-  s_local[d] = local_excl;
-  const uint64_t excl = lookback(status, tile, d, 256, cnt);
-  s_gbase[d] = (int64_t)pass_offset[d] + (int64_t)excl - (int64_t)local_excl;
+  // fold the tile-local digit offset into every warp's prefix: pos = s_whist[warp][d] + rank
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) s_whist[w * 256 + d] += local_excl;
+  // publish this tile's counts before doing local work so successors can proceed
+  uint64_t* mine = status + (uint64_t)tile * 256 + d;
+  st_relaxed(mine, (tile == 0 ? kFlagPrefix : kFlagAgg) | cnt);
   __syncthreads();
 
+  // stage the tile in digit order in shared memory (needs only tile-local offsets) ...
 #pragma unroll
   for (int i = 0; i < kIpt; ++i) {
     const uint64_t idx = wbase + i * 32 + lane;
     if (idx < n) {
       const unsigned dd = (unsigned)(key[i] >> shift) & dmask;
-      const uint32_t pos = s_local[dd] + s_whist[warp * 256 + dd] + rank[i];
+      const uint32_t pos = s_whist[warp * 256 + dd] + rank[i];
       s_keys[pos] = key[i];
       s_vals[pos] = val[i];
     }
   }
+  // ... then resolve the global offsets by look-back (overlapping predecessors' progress)
+  const uint64_t excl = lookback_published(status, tile, d, 256, cnt);
+  s_gbase[d] = (int64_t)pass_offset[d] + (int64_t)excl - (int64_t)local_excl;
   __syncthreads();
   const uint32_t valid_n = (n - base) < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
   for (uint32_t j = tid; j < valid_n; j += kThreads) {
@@ -315,10 +347,10 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, V* vals, V* vals_alt,
   rs_histogram<<<hblocks, 256, 0, s>>>(keys, n, begin_bit, end_bit, npasses, hist);
   rs_hist_scan<<<npasses, 256, 0, s>>>(hist);
 
-  const uint64_t tiles = (n + kTile - 1) / kTile;
+  const uint64_t tiles = (n + OneSweep<V>::TILE - 1) / OneSweep<V>::TILE;
   uint64_t* status = arena.alloc_n<uint64_t>(tiles * 256 + 8);
   uint32_t* counter = reinterpret_cast<uint32_t*>(status + tiles * 256);
-  constexpr size_t smem = onesweep_smem<V>();
+  constexpr size_t smem = OneSweep<V>::SMEM;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(rs_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,0 +1,89 @@
+"""Full-size parity at BASELINE configs[1] (R-MAT scale 22, 65.2M nonzeros) on the GPU.
+
+* Every conversion is BIT-EXACT: all storage_report arrays of all 11 engines equal the arrays
+  recomputed from the documented sort keys by the independent torch restatement
+  (tests/fullsize_ref.py, itself pinned to the C oracle in test_fullsize_ref_cpu.py).
+* Every engine's y is within 1e-12 * sum|a_ij x_j| of a fp64 scatter-add reference.
+* With integer values and x = 1 every engine's y is bitwise equal to the exact row sums
+  (the reference's integer-exact property, tests/test_parallel_spmv.cpp:374-392)."""
+import numpy as np
+import pytest
+import torch
+
+import fullsize_ref as fr
+
+pytestmark = pytest.mark.gpu
+
+NAMES = {0: "crs", 3: "csb", 4: "csbh", 5: "bcoh", 6: "bcohc", 7: "bcohch", 8: "bcohchp", 9: "mergeb",
+         10: "mergebh"}
+P = 8  # BCOH bands
+
+
+@pytest.fixture(scope="module")
+def cfg2(cuda):
+    from paper_2502_19284_b200 import gen
+    m, n, r, c, v = gen.rmat_device(22, 16, seed=1)
+    return m, n, r, c, v
+
+
+def _expected(sp, alg, m, n, r, c, v, lb):
+    if alg <= 2:
+        return fr.crs(m, r, c, v)
+    if alg in (3, 4):
+        return fr.csb(m, n, r, c, v, lb, alg == 4)
+    if alg in (9, 10):
+        return fr.mergeb(m, n, r, c, v, lb, alg == 10)
+    prefix = np.zeros(m + 1, dtype=np.uint64)
+    prefix[1:] = np.cumsum(torch.bincount(r.long(), minlength=m).cpu().numpy())
+    bounds = sp.partition_rows_by_nnz(prefix.astype(np.uint32), P, lb).tolist()
+    return fr.bcoh(m, n, r, c, v, lb, bounds, NAMES[alg])
+
+
+@pytest.mark.parametrize("alg", [0, 3, 4, 5, 6, 7, 8, 9, 10])
+def test_conversion_bit_exact_full_size(cuda, cfg2, alg):
+    sp = cuda
+    m, n, r, c, v = cfg2
+    f = sp.build_format(alg, sp.TripletMatrix(m, n, r, c, v), P)
+    exp = _expected(sp, alg, m, n, r, c, v, f.info["log2_beta"])
+    for a in sp.storage_report(f).arrays:
+        got = f.array(a.name)
+        want = fr.as_numpy_like(got, exp[a.name])
+        assert got.shape == want.shape, (NAMES[alg], a.name, got.shape, want.shape)
+        cmp = got.astype(np.float64) if got.dtype == np.float64 else got.astype(np.int64)
+        assert np.array_equal(cmp, want), f"{NAMES[alg]}: {a.name} differs at full size"
+        del got, want, cmp
+    del f, exp
+    torch.cuda.empty_cache()
+
+
+def test_all_engines_y_full_size(cuda, cfg2):
+    sp = cuda
+    m, n, r, c, v = cfg2
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3)) * 2 - 1
+    y_ref = torch.zeros(m, dtype=torch.float64, device="cuda")
+    y_ref.index_add_(0, r.long(), v * x[c.long()])
+    bound = torch.zeros(m, dtype=torch.float64, device="cuda")
+    bound.index_add_(0, r.long(), (v * x[c.long()]).abs())
+    a = sp.TripletMatrix(m, n, r, c, v)
+    for alg in range(11):
+        f = sp.build_format(alg, a, P)
+        y = sp.run_spmv(alg, f, x, p=P)
+        err = (y - y_ref).abs()
+        # y_ref itself carries summation error ~ n_row * eps * bound; both within 1e-12 * bound
+        assert bool((err <= 1e-12 * bound).all()), f"{sp.algorithm_name(alg)}: max {float((err / bound.clamp_min(1e-300)).max())}"
+        del f
+
+
+def test_integer_exact_full_size(cuda, cfg2):
+    sp = cuda
+    m, n, r, c, v = cfg2
+    vi = ((r.long() * 131 + c.long() * 7) % 5 + 1).double()
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    y_ref = torch.zeros(m, dtype=torch.float64, device="cuda")
+    y_ref.index_add_(0, r.long(), vi)
+    a = sp.TripletMatrix(m, n, r, c, vi)
+    for alg in range(11):
+        f = sp.build_format(alg, a, P)
+        y = sp.run_spmv(alg, f, ones, p=P)
+        assert bool((y == y_ref).all()), sp.algorithm_name(alg)
+        del f
