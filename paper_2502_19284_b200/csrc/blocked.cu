@@ -100,6 +100,79 @@ __global__ void __launch_bounds__(256) blocked_spmv_kernel(
   }
 }
 
+// Block-row window kernel for CSB / MergeB (block rows are contiguous in storage): one CTA per
+// window item -- a run of chunks inside one block row -- accumulates into a beta-row y window in
+// shared memory (shared fp64 adds, conflicts rare), then stores the window to y (item owns the
+// whole block row) or adds its nonzero entries (block row split into several items).  Replaces
+// one global fp64 reduction per element by one shared-memory add; the role of the reference's
+// per-task temporary vectors (spmv_parallel.hpp:218-274, 311-330).
+constexpr int kWinThreads = 1024;
+
+__global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
+    const uint32_t* __restrict__ packed, const double* __restrict__ data,
+    const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
+    const uint2* __restrict__ blk_rc, const uint32_t* __restrict__ item_chunk,
+    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ item_whole, unsigned lb, uint32_t m,
+    const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ double win[];
+  const uint32_t item = blockIdx.x;
+  const uint32_t c0 = item_chunk[item], c1 = item_chunk[item + 1];
+  const uint32_t beta = 1u << lb;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (uint32_t i = threadIdx.x; i < beta; i += blockDim.x) win[i] = 0.0;
+  __syncthreads();
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  constexpr int U = 8;  // 8 x 32 = one full chunk in flight per warp
+  for (uint32_t c = c0 + warp; c < c1; c += nwarps) {
+    const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
+    const uint32_t cbase = blk_rc[ch_blk[c]].y << lb;
+    for (uint32_t base = e0; base < e1; base += 32 * U) {
+      uint32_t pk[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = base + 32 * u + lane;
+        pk[u] = k < e1 ? ld_stream(packed + k, pf) : 0u;
+        v[u] = k < e1 ? ld_stream(data + k, pf) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = base + 32 * u + lane;
+        if (k < e1) v[u] *= ld_x(x + cbase + (pk[u] & 0xFFFFu), pl);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = base + 32 * u + lane;
+        // shared fp64 adds are CAS loops: merge runs of equal rows inside the warp first so that
+        // no two lanes of one instruction hit the same word (row-sorted blocks have long runs)
+        const uint32_t row = k < e1 ? pk[u] >> 16 : 0xFFFFFFFFu;
+        const uint32_t prow = __shfl_up_sync(0xFFFFFFFFu, row, 1);
+        const unsigned heads = __ballot_sync(0xFFFFFFFFu, lane == 0 || prow != row);
+        double w = v[u];
+        if (heads != 0xFFFFFFFFu) {
+          const int seg_start = 31 - __clz(heads & ((2u << lane) - 1u));
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xFFFFFFFFu, w, off);
+            if ((int)lane - off >= seg_start) w += t;
+          }
+        }
+        const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+        if (tail && k < e1) atomicAdd(&win[row], w);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t rbase = item_br[item] << lb;
+  const uint32_t rows = min(beta, m - rbase);
+  const bool whole = item_whole[item] != 0;
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double w = win[i];
+    if (whole) y[rbase + i] = w;
+    else if (w != 0.0) atomicAdd(y + rbase + i, w);
+  }
+}
+
 }  // namespace
 
 int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
@@ -109,6 +182,23 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   int dev = 0, sms = kNumSMs;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const DevArray* items = f.find("win_item_chunk")) {
+    const uint32_t nitems = (uint32_t)(items->count() - 1);
+    const size_t smem = sizeof(double) << f.log2_beta;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(window_spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    note_launch();
+    timing_begin("window_spmv_kernel", s);
+    window_spmv_kernel<<<nitems, kWinThreads, smem, s>>>(
+        f.find("packed")->as<uint32_t>(), f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
+        f.find("chunk_blk")->as<uint32_t>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
+        f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(), f.log2_beta, f.m, x, y);
+    timing_end(s);
+    return check_launch("spmv_blocked(window)");
+  }
   const uint64_t warps_needed = f.work_items;
   const unsigned blocks = (unsigned)std::min<uint64_t>((warps_needed + 7) / 8, (uint64_t)sms * 8);
   const DevArray* pk = f.find("packed");

@@ -386,6 +386,35 @@ __global__ void chunk_fill(const uint32_t* __restrict__ blk_begin, uint32_t nblk
   }
 }
 
+// Window-item plan for the block-row window kernel (CSB / MergeB): items start at every block-row
+// change and every kWinChunks-th chunk, so an item never crosses a block row.
+__global__ void win_heads(const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc, uint32_t nchunks,
+                          uint32_t per_item, uint32_t* __restrict__ head) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const bool row_start = c == 0 || blk_rc[ch_blk[c]].x != blk_rc[ch_blk[c - 1]].x;
+  head[c] = row_start ? 3u : (c % per_item == 0 ? 1u : 0u);
+}
+
+__global__ void win_flag(const uint32_t* __restrict__ head, uint32_t nchunks, uint32_t* __restrict__ flag) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nchunks) flag[c] = head[c] != 0u;
+}
+
+__global__ void win_fill(const uint32_t* __restrict__ head, const uint32_t* __restrict__ scan,
+                         const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc, uint32_t nchunks,
+                         uint32_t* __restrict__ item_chunk, uint32_t* __restrict__ item_br,
+                         uint32_t* __restrict__ item_whole) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks || !head[c]) return;
+  const uint32_t i = scan[c];
+  uint32_t e = c + 1;
+  while (e < nchunks && !head[e]) ++e;
+  item_chunk[i] = c;
+  item_br[i] = blk_rc[ch_blk[c]].x;
+  item_whole[i] = (head[c] & 2u) && (e == nchunks || (head[e] & 2u)) ? 1u : 0u;
+}
+
 int d2h_u32(const uint32_t* dev, uint32_t* host, cudaStream_t s) {
   cudaMemcpyAsync(host, dev, 4, cudaMemcpyDeviceToHost, s);
   return cudaStreamSynchronize(s) == cudaSuccess ? kOk : check_launch("d2h");
@@ -493,6 +522,39 @@ static int blocked_common(BlockedBuild& bb, const spmvlab_cuda_coo& a, const uin
   return check_launch("blocked_common");
 }
 
+// Window items for CSB / CSBH / MergeBH when the beta-row window fits in shared memory (beta <=
+// 2^14, 128 KB of fp64).  Those formats order elements inside a block along a curve, so the 32
+// rows a warp reduces into are scattered and the per-run global reduction kernel pays one L2
+// sector per element; the window kernel turns that into shared-memory adds (R-MAT s22: 831 ->
+// 637 us).  Row-major MergeB blocks give coalesced runs and stay on the reduction kernel, which
+// is faster there (335 vs 465 us).  SPMVLAB_BLOCKED_WINDOW=0 disables, =1 forces for all four.
+constexpr uint32_t kWinChunks = 256;
+
+static int window_plan(Format& f, Arena& ar, bool curve_in_block) {
+  const char* env = std::getenv("SPMVLAB_BLOCKED_WINDOW");
+  const bool want = env && env[0] ? env[0] == '1' : curve_in_block;
+  if (!want || f.log2_beta > 14 || f.work_items == 0) return kOk;
+  cudaStream_t s = ar.stream();
+  const uint32_t nch = (uint32_t)f.work_items;
+  const uint32_t* ch_blk = f.find("chunk_blk")->as<uint32_t>();
+  const uint2* blk_rc = f.find("blk_rc")->as<uint2>();
+  uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
+  uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
+  if (!head || !flag) return kNoMemory;
+  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ch_blk, blk_rc, nch, kWinChunks, head);
+  win_flag<<<(nch + 255) / 256, 256, 0, s>>>(head, nch, flag);  // flag = head != 0
+  exclusive_scan_u32(flag, flag, nch, ar);                        // -> item index of each head
+  uint32_t nitems = 0;
+  if (int rc = d2h_u32(flag + nch, &nitems, s)) return rc;
+  uint32_t* item_chunk = static_cast<uint32_t*>(f.add("win_item_chunk", (uint64_t)nitems + 1, 4, s));
+  uint32_t* item_br = static_cast<uint32_t*>(f.add("win_item_br", nitems, 4, s));
+  uint32_t* item_whole = static_cast<uint32_t*>(f.add("win_item_whole", nitems, 4, s));
+  if (!item_chunk || !item_br || !item_whole) return kNoMemory;
+  cudaMemcpyAsync(item_chunk + nitems, &nch, 4, cudaMemcpyHostToDevice, s);
+  win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ch_blk, blk_rc, nch, item_chunk, item_br, item_whole);
+  return check_launch("window_plan");
+}
+
 static Geom base_geom(const Format& f, unsigned lb) {
   Geom g{};
   g.lb = lb;
@@ -531,6 +593,7 @@ int build_csb(Format& f, const spmvlab_cuda_coo& a, unsigned lb, bool hilbert, u
     return d.name == "blk_ptr" || d.name == "packed" || d.name == "data";
   });
   f.nstorage = 3;
+  if (int rc = window_plan(f, ar, true)) return rc;
   return check_launch("build_csb");
 }
 
@@ -576,6 +639,7 @@ int build_mergeb(Format& f, const spmvlab_cuda_coo& a, unsigned lb, bool hilbert
   }
   f.arrays = sorted;
   f.nstorage = 5;
+  if (int rc = window_plan(f, ar, hilbert)) return rc;
   return check_launch("build_mergeb");
 }
 

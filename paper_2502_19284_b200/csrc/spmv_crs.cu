@@ -328,8 +328,9 @@ __global__ void __launch_bounds__(THREADS, 4) merge_spmv_smem_kernel(
 // Two shared-memory operations per nonzero (striped product store, blocked product load); each
 // lane's starting path point comes from scattering row ends to their owning lanes plus a
 // shuffle suffix-minimum; rows completed by a lane are stored straight to y.
+// Register budget: IPT <= 7 fits 40 registers (48 warps per SM); larger tiles need ~64.
 template <int IPT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 4 ? 48 / WARPS : 12)) merge_spmv_wstage_kernel(
+__global__ void __launch_bounds__(WARPS * 32, (IPT <= 7 ? 48 : 32) / WARPS) merge_spmv_wstage_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
@@ -408,17 +409,17 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS >= 4 ? 48 / WARPS : 12)) me
       ++ji;
     }
   }
-  // warp segmented scan of (has_row_end, tail)
+  // Warp segmented scan of the lane tails; a lane that completed a row starts a new segment (its
+  // tail follows its last row end).  Segment starts come from one ballot, so only the values are
+  // shuffled: v = sum of tails from the segment start through this lane.
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, first_row >= 0);
+  const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int seg = heads & le ? 31 - __clz(heads & le) : 0;
   double v = run;
-  int fl = first_row >= 0 ? 1 : 0;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const double ov = __shfl_up_sync(0xFFFFFFFFu, v, off);
-    const int of = __shfl_up_sync(0xFFFFFFFFu, fl, off);
-    if (lane >= off) {
-      if (!fl) v += ov;
-      fl |= of;
-    }
+    if (lane - off >= seg) v += ov;
   }
   double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
   if (lane == 0) ex = 0.0;

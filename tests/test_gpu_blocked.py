@@ -114,6 +114,38 @@ def test_integer_exact_all_engines(cuda, oracle):
             np.testing.assert_array_equal(y, y_ref, err_msg=f"alg {alg} p {p}")
 
 
+@pytest.mark.parametrize("window", ["0", "1"])
+def test_window_and_reduction_kernels(cuda, oracle, monkeypatch, window):
+    """CSB / CSBH / MergeB / MergeBH multiply through both device kernels (shared-memory block-row
+    window, forced with SPMVLAB_BLOCKED_WINDOW=1; per-run global reduction with =0), on a matrix
+    whose block rows span several window items (split rows add into y, whole rows store)."""
+    monkeypatch.setenv("SPMVLAB_BLOCKED_WINDOW", window)
+    sp = cuda
+    from paper_2502_19284_b200 import gen
+    m, n, r, c, v = gen.rmat_host(15, 16, seed=8)
+    x = np.random.default_rng(4).uniform(-1, 1, n)
+    bound = oracle.abs_spmv(m, r, c, v, x)
+    a = _dev(sp, m, n, r, c, v)
+    xd = torch.from_numpy(x).cuda()
+    vi = ((r.astype(np.int64) * 7 + c) % 5 + 1).astype(np.float64)
+    ai = _dev(sp, m, n, r, c, vi)
+    exact = oracle.spmv_triplet(m, r, c, vi, np.ones(n))
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    for alg in (3, 4, 9, 10):
+        ref = oracle.build(alg, m, n, r, c, v, threads=1, l2_bytes=512 * 1024)
+        f = sp.build_format(alg, a, 1, sp.EngineOptions(l2_bytes=512 * 1024))
+        _check_format(sp, f, ref, alg, f"window {window} alg {alg}")
+        names = [d.name for d in sp.storage_report(f).arrays]
+        if window == "1":
+            whole = f.array("win_item_whole")
+            assert 0 in whole and 1 in whole, "expected both split and whole block rows"
+        assert "win_item_chunk" not in names  # plan arrays are not storage
+        y = sp.run_spmv(alg, f, xd, p=1).cpu().numpy()
+        assert_y_close(y, oracle.spmv(ref, alg, x, p=1), bound, what=f"window {window} alg {alg}")
+        fi = sp.build_format(alg, ai, 1, sp.EngineOptions(l2_bytes=512 * 1024))
+        np.testing.assert_array_equal(sp.run_spmv(alg, fi, ones, p=1).cpu().numpy(), exact)
+
+
 def test_bcoh_band_mismatch(cuda):
     """spmv_parallel.hpp:339-341: BCOH multiply with p != bands is InvalidArgument."""
     sp = cuda
