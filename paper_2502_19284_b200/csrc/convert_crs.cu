@@ -86,6 +86,18 @@ __global__ void merge_path_search_kernel(const uint32_t* __restrict__ a, uint64_
   out_i[k] = lo;
 }
 
+__global__ void long_row_flags(const uint32_t* __restrict__ row_ptr, uint32_t m, uint32_t lim,
+                               uint32_t* __restrict__ flag) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) flag[r] = row_ptr[r + 1] - row_ptr[r] > lim;
+}
+
+__global__ void long_row_fill(const uint32_t* __restrict__ row_ptr, uint32_t m, uint32_t lim,
+                              const uint32_t* __restrict__ scan, uint32_t* __restrict__ out) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m && row_ptr[r + 1] - row_ptr[r] > lim) out[scan[r]] = r;
+}
+
 }  // namespace
 
 int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar) {
@@ -153,6 +165,20 @@ int build_merge_plan(Format& f, Arena& ar) {
   uint32_t g = 2;
   while (g < 32 && g < mean) g <<= 1;
   f.par_group = g;
+  // ParCRS long rows (> kParLongIters * g nonzeros) get one CTA each; the rest stay with the groups.
+  const uint32_t lim = kParLongIters * g;
+  uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)f.m + 1);
+  if (!flag) return kNoMemory;
+  if (f.m) long_row_flags<<<(f.m + 255) / 256, 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, lim, flag);
+  exclusive_scan_u32(flag, flag, f.m, ar);
+  uint32_t nlong = 0;
+  cudaMemcpyAsync(&nlong, flag + f.m, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan");
+  uint32_t* lr = static_cast<uint32_t*>(f.add("par_long_rows", nlong, 4, s));
+  if (nlong && !lr) return kNoMemory;
+  if (nlong)
+    long_row_fill<<<(f.m + 255) / 256, 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, lim, flag, lr);
+  f.par_long = nlong;
   return check_launch("build_merge_plan");
 }
 

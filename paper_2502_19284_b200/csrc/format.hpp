@@ -41,6 +41,7 @@ struct spmvlab_cuda_format {
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;
+  uint32_t par_long = 0;  // ParCRS rows with > kParLongRow nonzeros ("par_long_rows")
 
   // ---- blocked plan (CSB / MergeB / BCOH): work items = (element range, y window)
   uint32_t work_items = 0;

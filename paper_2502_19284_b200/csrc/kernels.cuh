@@ -20,6 +20,9 @@ constexpr int kVariantWarpStage = 3;
 constexpr int kMergeThreads = 256;
 constexpr int kMergeIpt = 7;
 constexpr int kMergeVariant = kVariantWarpStage;
+// ParCRS: rows longer than kParLongIters * group width are summed by a whole CTA (a sub-warp group
+// would walk them serially -- R-MAT s22 row 0 has ~10^5 nonzeros); those CTAs come first in the grid.
+constexpr uint32_t kParLongIters = 32;
 bool merge_shape_supported(int threads, int ipt, int variant);
 uint32_t merge_tile_items(int threads, int ipt, int variant);
 

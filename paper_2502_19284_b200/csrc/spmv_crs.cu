@@ -37,32 +37,109 @@ namespace spmvcu {
 extern thread_local std::string g_last_error;
 namespace {
 
-__global__ void seq_crs_kernel(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
-                               const double* __restrict__ val, const double* __restrict__ x,
-                               double* __restrict__ y, uint32_t m) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// The first nlong CTAs each own one long row: all threads form the rounded products of the next
+// 2048-element chunk in shared memory while thread 0 adds the current chunk in storage order
+// (double buffered), so the sum is the reference's left-to-right chain.  The other CTAs run one
+// thread per short row with 8 products in flight ahead of the sequential adds.
+constexpr int kSeqThreads = 256;
+constexpr int kSeqChunk = 2048;
+
+__global__ void __launch_bounds__(kSeqThreads) seq_crs_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, uint32_t m, const uint32_t* __restrict__ long_rows,
+    uint32_t nlong, uint32_t lim) {
+  if (blockIdx.x < nlong) {
+    __shared__ double prod[2][kSeqChunk];
+    const uint32_t r = long_rows[blockIdx.x];
+    const uint32_t b = row_ptr[r], e = row_ptr[r + 1];
+    const uint32_t nch = (e - b + kSeqChunk - 1) / kSeqChunk;
+    auto fill = [&](uint32_t c) {
+      const uint32_t base = b + c * kSeqChunk;
+#pragma unroll
+      for (int u = 0; u < kSeqChunk / kSeqThreads; ++u) {
+        const uint32_t k = base + u * kSeqThreads + threadIdx.x;
+        if (k < e) prod[c & 1][u * kSeqThreads + threadIdx.x] = __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k)));
+      }
+    };
+    fill(0);
+    __syncthreads();
+    double sum = 0.0;
+    for (uint32_t c = 0; c < nch; ++c) {
+      if (c + 1 < nch) fill(c + 1);
+      if (threadIdx.x == 0) {
+        const uint32_t cnt = min((uint32_t)kSeqChunk, e - b - c * kSeqChunk);
+        const double* p = prod[c & 1];
+#pragma unroll 16
+        for (uint32_t i = 0; i < cnt; ++i) sum = __dadd_rn(sum, p[i]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) y[r] = sum;
+    return;
+  }
+  const uint32_t i = (blockIdx.x - nlong) * blockDim.x + threadIdx.x;
   if (i >= m) return;
+  const uint32_t b = row_ptr[i], e = row_ptr[i + 1];
+  if (e - b > lim) return;  // owned by a long-row CTA
   double sum = 0.0;
-  const uint32_t e = row_ptr[i + 1];
-  for (uint32_t k = row_ptr[i]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(val[k], x[col[k]]));
+  uint32_t k = b;
+  for (; k + 8 <= e; k += 8) {
+    double p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(__ldg(val + k + u), __ldg(x + __ldg(col + k + u)));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, p[u]);
+  }
+  for (; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
   y[i] = sum;
 }
 
+// The first nlong CTAs each sum one long row (4 independent strided partials per thread, then a
+// CTA reduction); the remaining CTAs run the sub-warp groups over all other rows.
 template <int G>
 __global__ void __launch_bounds__(256) par_crs_kernel(const uint32_t* __restrict__ row_ptr,
                                                       const uint32_t* __restrict__ col,
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ x,
-                                                      double* __restrict__ y, uint32_t m) {
-  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                      double* __restrict__ y, uint32_t m,
+                                                      const uint32_t* __restrict__ long_rows, uint32_t nlong,
+                                                      uint32_t lim) {
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  const unsigned lane = threadIdx.x & 31u;
+  if (blockIdx.x < nlong) {
+    __shared__ double part[8];
+    const uint32_t r = long_rows[blockIdx.x];
+    const uint32_t b = row_ptr[r], e = row_ptr[r + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    uint32_t k = b + threadIdx.x;
+    for (; k + 768 < e; k += 1024) {
+      s0 += ld_stream(val + k, pf) * ld_x(x + ld_stream(col + k, pf), pl);
+      s1 += ld_stream(val + k + 256, pf) * ld_x(x + ld_stream(col + k + 256, pf), pl);
+      s2 += ld_stream(val + k + 512, pf) * ld_x(x + ld_stream(col + k + 512, pf), pl);
+      s3 += ld_stream(val + k + 768, pf) * ld_x(x + ld_stream(col + k + 768, pf), pl);
+    }
+    for (; k < e; k += 256) s0 += ld_stream(val + k, pf) * ld_x(x + ld_stream(col + k, pf), pl);
+    double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+    if (lane == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += part[w];
+      y[r] = t;
+    }
+    return;
+  }
+  const uint64_t gid = (uint64_t)(blockIdx.x - nlong) * blockDim.x + threadIdx.x;
   const uint32_t sub = threadIdx.x & (G - 1);
   const uint64_t group = gid / G;
-  const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / G;
-  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t ngroups = (uint64_t)(gridDim.x - nlong) * blockDim.x / G;
   const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(unsigned)(G - 1)));
-  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   for (uint64_t r = group; r < m; r += ngroups) {
     const uint32_t b = row_ptr[r], e = row_ptr[r + 1];
+    if (e - b > lim) continue;  // group-uniform: a long-row CTA owns it
     double s = 0.0;
     for (uint32_t k = b + sub; k < e; k += G) s += ld_stream(val + k, pf) * ld_x(x + ld_stream(col + k, pf), pl);
 #pragma unroll
@@ -619,10 +696,13 @@ void launch_merge_tma(const Format& f, const double* x, double* y, const Scratch
 
 int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.m == 0) return kOk;
+  const DevArray* lra = f.find("par_long_rows");
+  const uint32_t* lr = lra ? lra->as<uint32_t>() : nullptr;
+  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? kParLongIters * f.par_group : 0xFFFFFFFFu;
   timing_begin("seq_crs_kernel", s);
-  seq_crs_kernel<<<(f.m + 127) / 128, 128, 0, s>>>(f.find("row_ptr")->as<uint32_t>(),
-                                                   f.find("col_ind")->as<uint32_t>(),
-                                                   f.find("data")->as<double>(), x, y, f.m);
+  seq_crs_kernel<<<(f.m + kSeqThreads - 1) / kSeqThreads + nl, kSeqThreads, 0, s>>>(
+      f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(), x, y,
+      f.m, lr, nl, lim);
   timing_end(s);
   note_launch();
   return check_launch("spmv_seq_crs");
@@ -633,15 +713,20 @@ int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
   const uint32_t* ci = f.find("col_ind")->as<uint32_t>();
   const double* d = f.find("data")->as<double>();
-  const unsigned blocks = grid_for((uint64_t)f.m * f.par_group, 256, kNumSMs * 8);
+  const unsigned blocks = grid_for((uint64_t)f.m * f.par_group, 256, kNumSMs * 8) + f.par_long;
+  const DevArray* lra = f.find("par_long_rows");
+  const uint32_t* lr = lra ? lra->as<uint32_t>() : nullptr;
+  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? kParLongIters * f.par_group : 0xFFFFFFFFu;
   note_launch();
+  timing_begin("par_crs_kernel", s);
   switch (f.par_group) {
-    case 2: par_crs_kernel<2><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
-    case 4: par_crs_kernel<4><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
-    case 8: par_crs_kernel<8><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
-    case 16: par_crs_kernel<16><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
-    default: par_crs_kernel<32><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m); break;
+    case 2: par_crs_kernel<2><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m, lr, nl, lim); break;
+    case 4: par_crs_kernel<4><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m, lr, nl, lim); break;
+    case 8: par_crs_kernel<8><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m, lr, nl, lim); break;
+    case 16: par_crs_kernel<16><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m, lr, nl, lim); break;
+    default: par_crs_kernel<32><<<blocks, 256, 0, s>>>(rp, ci, d, x, y, f.m, lr, nl, lim); break;
   }
+  timing_end(s);
   return check_launch("spmv_par_crs");
 }
 

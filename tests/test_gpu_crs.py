@@ -102,6 +102,10 @@ def test_merge_long_rows_and_empty_rows(cuda, oracle):
     assert_y_close(y, y_ref, bound, what="merge long rows")
     y = sp.run_spmv(1, f, torch.from_numpy(x).cuda(), p=1).cpu().numpy()
     assert_y_close(y, y_ref, bound, what="parcrs long rows")
+    # SeqCrs long rows go to one CTA each (chunked products, one ordered add chain): still bitwise
+    y = sp.run_spmv(0, f, torch.from_numpy(x).cuda(), p=1).cpu().numpy()
+    np.testing.assert_array_equal(y, y_ref)
+    assert f.array("par_long_rows").tolist() == [7, 8, 49999]
 
 
 def test_cfg1_er_crs(cuda, oracle):

@@ -74,6 +74,21 @@ def test_all_engines_y_full_size(cuda, cfg2):
         del f
 
 
+def test_seq_crs_bitwise_full_size(cuda, oracle, cfg2):
+    """SeqCrs at full size is BITWISE equal to the reference's sequential row sums: the C oracle's
+    entry-order spmv_triplet over the (bit-exact) CRS order is the same left-to-right chain."""
+    sp = cuda
+    m, n, r, c, v = cfg2
+    f = sp.build_format(0, sp.TripletMatrix(m, n, r, c, v), 1)
+    rp = f.array("row_ptr")
+    rows = np.repeat(np.arange(m, dtype=np.uint32), np.diff(rp.astype(np.int64)))
+    x = np.random.default_rng(12).uniform(-1, 1, n)
+    y = sp.run_spmv(0, f, torch.from_numpy(x).cuda(), p=1).cpu().numpy()
+    want = oracle.spmv_triplet(m, rows, f.array("col_ind"), f.array("data"), x)
+    np.testing.assert_array_equal(y, want)
+    assert len(f.array("par_long_rows")) > 0  # the long-row CTA path ran
+
+
 def test_integer_exact_full_size(cuda, cfg2):
     sp = cuda
     m, n, r, c, v = cfg2
