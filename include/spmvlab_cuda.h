@@ -87,6 +87,20 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
                                const spmvlab_cuda_options* opt, double* x_dev, double* y_dev,
                                void* stream);
 
+/* Iterated multiply x_{k+1} = A x_k (square A), `iters` times: the cfg5 application loop around
+ * run_spmv (BASELINE configs[4], "x <- A x for 100 iterations"; the reference has no loop of its
+ * own, its caller repeats inc/engine.hpp:126-148).  x (device, n) holds x_0 on entry and x_iters on
+ * return; work is a device buffer of n doubles.  With SPMVLAB_ITER_NORMALIZE each iterate is
+ * rescaled to unit L1 mass.  If `norms` (device, 2 * iters doubles) is non-NULL, iteration k writes
+ * norms[2k] = ||x_{k+1} - x_k||_1 and norms[2k+1] = sum_i (A x_k)_i, the mass before any rescale
+ * (its drop from the previous mass is the leakage through empty columns), both by deterministic
+ * fixed-order reductions.  SPMVLAB_ITER_GRAPH captures the whole loop as one CUDA graph and
+ * launches it once (requires a non-default stream). */
+#define SPMVLAB_ITER_NORMALIZE 1
+#define SPMVLAB_ITER_GRAPH 2
+int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, double* work, uint32_t iters,
+                         unsigned p, int flags, double* norms, void* stream);
+
 /* storage_report(const BuiltFormat&) -- inc/engine.hpp:158-160 / inc/storage.hpp:62-123. */
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,
                                 size_t capacity, size_t* count);

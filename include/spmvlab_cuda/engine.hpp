@@ -231,6 +231,15 @@ inline void run_spmv_device(Algorithm alg, const BuiltFormat& f, const double* x
   check(spmvlab_cuda_run_spmv(static_cast<int>(alg), f.handle(), x_dev, x_len, y_dev, y_len, p, &o, stream));
 }
 
+// The cfg5 application loop x <- A x (spmvlab_cuda_iterate): x_dev in/out, work_dev n doubles,
+// norms_dev NULL or 2 * iters doubles; stream-ordered (graph=true needs a non-default stream).
+inline void iterate_device(Algorithm alg, const BuiltFormat& f, double* x_dev, double* work_dev, std::uint32_t iters,
+                           unsigned p, bool normalize = false, bool graph = false, double* norms_dev = nullptr,
+                           cudaStream_t stream = nullptr) {
+  const int flags = (normalize ? SPMVLAB_ITER_NORMALIZE : 0) | (graph ? SPMVLAB_ITER_GRAPH : 0);
+  check(spmvlab_cuda_iterate(static_cast<int>(alg), f.handle(), x_dev, work_dev, iters, p, flags, norms_dev, stream));
+}
+
 // run_spmv (inc/engine.hpp:126-148): host vectors, y fully overwritten, synchronous.
 template <typename Vec>
 void run_spmv(Algorithm alg, const BuiltFormat& f, const Vec& x, Vec& y, unsigned p, const EngineOptions& opt = {}) {

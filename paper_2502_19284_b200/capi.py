@@ -22,6 +22,7 @@ EXPORTS = [
     "spmvlab_cuda_curve_keys", "spmvlab_cuda_sort_pairs", "spmvlab_cuda_exclusive_scan",
     "spmvlab_cuda_launch_count", "spmvlab_cuda_kernel_timing", "spmvlab_cuda_kernel_time",
     "spmvlab_cuda_cache_read", "spmvlab_cuda_cache_write", "spmvlab_cuda_free_coo", "spmvlab_cuda_cache_info",
+    "spmvlab_cuda_iterate",
 ]
 
 
@@ -62,6 +63,7 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_last_error.restype = C.c_char_p
     L.spmvlab_cuda_build_format.argtypes = [i, C.POINTER(Coo), C.c_uint, C.POINTER(Options), C.POINTER(vp), vp]
     L.spmvlab_cuda_run_spmv.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp]
+    L.spmvlab_cuda_iterate.argtypes = [i, vp, vp, vp, u32, C.c_uint, i, vp, vp]
     L.spmvlab_cuda_run_spmv_host.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp, vp, vp]
     L.spmvlab_cuda_storage_report.argtypes = [vp, C.POINTER(StorageArray), C.c_size_t, C.POINTER(C.c_size_t)]
     L.spmvlab_cuda_get_format_info.argtypes = [vp, C.POINTER(FormatInfo)]

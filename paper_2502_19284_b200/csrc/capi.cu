@@ -120,6 +120,14 @@ void timing_end(cudaStream_t s) {
   ++t.launches;
 }
 
+bool timing_enable(bool on) {
+  KernelTimer& t = timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  const bool was = t.enabled;
+  t.enabled = on;
+  return was;
+}
+
 }  // namespace spmvcu
 
 using namespace spmvcu;
@@ -302,6 +310,46 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
   if (rc) return rc;
   if (y_len) cudaMemcpyAsync(y_host, y_dev, y_len * sizeof(double), cudaMemcpyDeviceToHost, s);
   return check_launch("run_spmv_host");
+}
+
+int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, double* work, uint32_t iters,
+                         unsigned p, int flags, double* norms, void* stream) {
+  if (!f) return fail(kInvalidArgument, "null format");
+  if (f->m != f->n) return fail(kDimensionMismatch, "iterate needs a square matrix");
+  if (f->n && (!x || !work)) return fail(kInvalidArgument, "null x or work buffer");
+  if (flags & ~(SPMVLAB_ITER_NORMALIZE | SPMVLAB_ITER_GRAPH)) return fail(kInvalidArgument, "unknown flags");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto mult = [&](const double* xi, double* yi, cudaStream_t st) {
+    return spmvlab_cuda_run_spmv(alg, f, xi, f->n, yi, f->m, p, nullptr, st);
+  };
+  if (!(flags & SPMVLAB_ITER_GRAPH) || iters == 0) return iterate(*f, mult, x, work, iters, flags, norms, s);
+  if (!s) return fail(kInvalidArgument, "graph mode needs a non-default stream");
+  // nothing may allocate synchronously inside the capture: create this stream's carry scratch now
+  if (alg == kMerge && is_crs_alg(f->alg) && !f->stream_scratch(s))
+    return fail(kNoMemory, "device allocation failed (merge carry scratch)");
+  const bool timing = timing_enable(false);
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    timing_enable(timing);
+    return check_launch("iterate(capture)");
+  }
+  const int rc = iterate(*f, mult, x, work, iters, flags, norms, s);
+  const cudaError_t ce = cudaStreamEndCapture(s, &g);
+  timing_enable(timing);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) return check_launch("iterate(capture)");
+  cudaGraphExec_t ge = nullptr;
+  if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return check_launch("iterate(instantiate)");
+  }
+  cudaGraphLaunch(ge, s);
+  cudaGraphExecDestroy(ge);  // freed once the in-flight launch completes
+  cudaGraphDestroy(g);
+  return check_launch("iterate(graph)");
 }
 
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <cuda_runtime.h>
 
 #include "../../include/spmvlab_cuda.h"
@@ -39,6 +40,11 @@ int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s);
 int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s);
 int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s);
 
+// ---- iterated multiply (iterate.cu): x <- A x, `iters` times, with optional norms / rescaling
+using SpmvFn = std::function<int(const double* x, double* y, cudaStream_t s)>;
+int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
+            double* norms, cudaStream_t s);
+
 // ---- primitives
 int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,
                       uint64_t count, uint64_t* out_i, cudaStream_t s);
@@ -53,6 +59,7 @@ int cache_write(const char* path, const spmvlab_cuda_coo& a, cudaStream_t s);
 void note_launch(unsigned n = 1);
 void timing_begin(const char* kernel, cudaStream_t s);  // no-op unless enabled
 void timing_end(cudaStream_t s);
+bool timing_enable(bool on);  // returns the previous state (graph capture suspends the brackets)
 
 inline unsigned grid_for(uint64_t n, unsigned threads, unsigned max_blocks = kNumSMs * 16) {
   uint64_t b = (n + threads - 1) / threads;

@@ -247,6 +247,36 @@ def run_spmv_host(alg, fmt: BuiltFormat, x_host: torch.Tensor, y_host: torch.Ten
     return y_host
 
 
+ITER_NORMALIZE = 1
+ITER_GRAPH = 2
+
+
+def iterate(alg, fmt: BuiltFormat, x: torch.Tensor, iters: int, p: int = 1, normalize: bool = False,
+            graph: bool = False, norms: bool = True, work: torch.Tensor | None = None, stream=None):
+    """x <- A x, `iters` times, in place on the device (the cfg5 application loop around
+    inc/engine.hpp:126-148).  Returns (x, norms) with norms a (iters, 2) device tensor of
+    (||x_{k+1} - x_k||_1, mass of A x_k) per iteration, or None.  graph=True runs the loop as one
+    CUDA graph on `stream` (a torch.cuda.Stream; the current stream if None)."""
+    if x.dtype != torch.float64:
+        raise Error(ErrorKind.InvalidArgument, "x must be float64")
+    if work is None:
+        work = torch.empty_like(x)
+    nb = torch.empty((iters, 2), dtype=torch.float64, device=x.device) if norms else None
+    flags = (ITER_NORMALIZE if normalize else 0) | (ITER_GRAPH if graph else 0)
+    cur = torch.cuda.current_stream(x.device)
+    st = stream if stream is not None else cur
+    side = None
+    if graph and _stream(st) == 0:  # graphs cannot be captured on the legacy default stream
+        side = torch.cuda.Stream(x.device)
+        side.wait_stream(st)
+        st = side
+    _check(capi.load().spmvlab_cuda_iterate(int(alg), fmt.handle, x.data_ptr(), work.data_ptr(), int(iters), int(p),
+                                            flags, nb.data_ptr() if nb is not None else None, _stream(st)))
+    if side is not None:
+        cur.wait_stream(side)
+    return x, nb
+
+
 _FORMAT_NAMES = {0: "crs", 1: "crs", 2: "crs", 3: "csb", 4: "csbh", 5: "bcoh", 6: "bcohc", 7: "bcohch",
                  8: "bcohchp", 9: "mergeb", 10: "mergebh"}
 

@@ -105,6 +105,32 @@ int main() {
   check_matrix(random_matrix(300, 250, 0.03, 11, 250), "rand300", 4096);
   check_matrix(random_matrix(1000, 1200, 0.01, 12), "rand1000", 512 * 1024);
   check_matrix(random_matrix(77, 5, 0.3, 13), "tall", 64);
+  // iterate_device: 10 SeqCrs iterations are bitwise the oracle's repeated sequential CRS multiply
+  {
+    TripletMatrix a = random_matrix(400, 400, 0.02, 14, 400);
+    for (double& v : a.data) v = std::fabs(v);
+    sc::BuiltFormat f = sc::build_format(sc::Algorithm::SeqCrs, a, 1);
+    orc_format* ref = nullptr;
+    orc_build_format(0, a.m, a.n, a.data.size(), a.row_ind.data(), a.col_ind.data(), a.data.data(), 1, 512 * 1024,
+                     &ref);
+    std::vector<double> x(a.n), y(a.n);
+    orc_verification_input(a.n, 9, x.data());
+    double *xd = nullptr, *wd = nullptr;
+    cudaMalloc(&xd, 8 * a.n);
+    cudaMalloc(&wd, 8 * a.n);
+    cudaMemcpy(xd, x.data(), 8 * a.n, cudaMemcpyHostToDevice);
+    sc::iterate_device(sc::Algorithm::SeqCrs, f, xd, wd, 10, 1);
+    std::vector<double> got(a.n);
+    cudaMemcpy(got.data(), xd, 8 * a.n, cudaMemcpyDeviceToHost);
+    for (int k = 0; k < 10; ++k) {
+      orc_run_spmv(0, ref, x.data(), x.size(), y.data(), y.size(), 1, 0);
+      std::swap(x, y);
+    }
+    EXPECT(got == x, "iterate_device SeqCrs x_10 differs from the oracle loop");
+    cudaFree(xd);
+    cudaFree(wd);
+    orc_free_format(ref);
+  }
   // errors: DimensionMismatch (spmv_parallel.hpp:90-99), band mismatch (:339-341)
   {
     sc::BuiltFormat f = sc::build_format(sc::Algorithm::Merge, e4, 1);
