@@ -94,8 +94,8 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
  * rescaled to unit L1 mass.  If `norms` (device, 2 * iters doubles) is non-NULL, iteration k writes
  * norms[2k] = ||x_{k+1} - x_k||_1 and norms[2k+1] = sum_i (A x_k)_i, the mass before any rescale
  * (its drop from the previous mass is the leakage through empty columns), both by deterministic
- * fixed-order reductions.  SPMVLAB_ITER_GRAPH captures the whole loop as one CUDA graph and
- * launches it once (requires a non-default stream). */
+ * fixed-order reductions.  SPMVLAB_ITER_GRAPH captures one iteration pair (x -> work -> x) as a
+ * CUDA graph and replays it iters / 2 times (requires a non-default stream). */
 #define SPMVLAB_ITER_NORMALIZE 1
 #define SPMVLAB_ITER_GRAPH 2
 int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, double* work, uint32_t iters,

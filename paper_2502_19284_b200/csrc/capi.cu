@@ -327,29 +327,10 @@ int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, doubl
   // nothing may allocate synchronously inside the capture: create this stream's carry scratch now
   if (alg == kMerge && is_crs_alg(f->alg) && !f->stream_scratch(s))
     return fail(kNoMemory, "device allocation failed (merge carry scratch)");
-  const bool timing = timing_enable(false);
-  cudaGraph_t g = nullptr;
-  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-    timing_enable(timing);
-    return check_launch("iterate(capture)");
-  }
+  const bool timing = timing_enable(false);  // no event brackets inside a capture
   const int rc = iterate(*f, mult, x, work, iters, flags, norms, s);
-  const cudaError_t ce = cudaStreamEndCapture(s, &g);
   timing_enable(timing);
-  if (rc) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
-  }
-  if (ce != cudaSuccess) return check_launch("iterate(capture)");
-  cudaGraphExec_t ge = nullptr;
-  if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
-    cudaGraphDestroy(g);
-    return check_launch("iterate(instantiate)");
-  }
-  cudaGraphLaunch(ge, s);
-  cudaGraphExecDestroy(ge);  // freed once the in-flight launch completes
-  cudaGraphDestroy(g);
-  return check_launch("iterate(graph)");
+  return rc;
 }
 
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,

@@ -7,8 +7,11 @@
 // norms ||x_{k+1} - x_k||_1 and the mass sum(x_{k+1}) -- the mass lost since the previous step is
 // the leakage through empty columns of the column-normalised matrix -- and optionally rescales
 // x_{k+1} to unit mass.  Reductions are deterministic: fixed per-CTA grid-stride partial sums, the
-// last CTA to finish (ticket counter) adds the partials in CTA order.  The loop can be captured
-// into one CUDA graph (no per-iteration launch latency for small matrices).
+// last CTA to finish (ticket counter) reduces the partials in a fixed tree order.
+//
+// Where the norms of iteration k go is decided on the device (an iteration counter in the scratch
+// block), so the launch parameters of every iteration pair (x -> work -> x) are identical: graph
+// mode captures ONE pair and replays it iters / 2 times.
 #include <algorithm>
 #include <string>
 #include <utility>
@@ -21,18 +24,50 @@ extern thread_local std::string g_last_error;
 namespace {
 
 constexpr int kRedThreads = 256;
-constexpr unsigned kRedBlocks = 2 * kNumSMs;
+constexpr unsigned kRedBlocks = 8 * kNumSMs;
+constexpr int kRedUnroll = 4;
 
-// mode bit 0: accumulate the mass of y; bit 1: scale y by 1 / *mass_in first; bit 2: accumulate
-// |y - x|.  out[0] = diff, out[1] = mass (only the accumulated ones are written).
+struct IterScratch {
+  double partial[2 * kRedBlocks];
+  double pair[2];    // (diff, mass) of the current iteration when the caller keeps no norms
+  unsigned ticket;   // CTAs finished in the current reduction
+  unsigned iter;     // iteration index (selects norms + 2 * iter)
+};
+
+__device__ __forceinline__ double* iter_out(IterScratch* sc, double* norms) {
+  return norms ? norms + 2ull * sc->iter : sc->pair;
+}
+
+// MODE bit 0: accumulate the mass of y; bit 1: scale y by 1 / (mass of this iteration) first;
+// bit 2: accumulate |y - x|.  Writes out[0] = diff, out[1] = mass (those accumulated); with
+// bit 3 (last reduction of the iteration) the iteration counter advances.
 template <int MODE>
-__global__ void __launch_bounds__(kRedThreads) iter_reduce_kernel(const double* __restrict__ x, double* __restrict__ y,
-                                                                  uint64_t n, const double* __restrict__ mass_in,
-                                                                  double* __restrict__ partial,
-                                                                  unsigned* __restrict__ ticket, double* __restrict__ out) {
-  const double scale = (MODE & 2) ? 1.0 / *mass_in : 1.0;
+__global__ void __launch_bounds__(kRedThreads) iter_reduce_kernel(const double* __restrict__ x,
+                                                                  double* __restrict__ y, uint64_t n,
+                                                                  IterScratch* sc, double* norms) {
+  double scale = 1.0;
+  if (MODE & 2) scale = 1.0 / iter_out(sc, norms)[1];
   double d = 0.0, s = 0.0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kRedUnroll - 1) * stride < n; i += kRedUnroll * stride) {
+    double v[kRedUnroll], xv[kRedUnroll];
+#pragma unroll
+    for (int u = 0; u < kRedUnroll; ++u) {
+      v[u] = y[i + u * stride];
+      if (MODE & 4) xv[u] = x[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < kRedUnroll; ++u) {
+      if (MODE & 2) {
+        v[u] *= scale;
+        y[i + u * stride] = v[u];
+      }
+      if (MODE & 1) s += v[u];
+      if (MODE & 4) d += fabs(v[u] - xv[u]);
+    }
+  }
+  for (; i < n; i += stride) {
     double v = y[i];
     if (MODE & 2) {
       v *= scale;
@@ -43,47 +78,69 @@ __global__ void __launch_bounds__(kRedThreads) iter_reduce_kernel(const double* 
   }
   __shared__ double sd[kRedThreads / 32], ss[kRedThreads / 32];
   __shared__ bool last;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    d += __shfl_xor_sync(0xFFFFFFFFu, d, off);
-    s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
-  }
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    sd[warp] = d;
-    ss[warp] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double bd = 0.0, bs = 0.0;
-    for (int w = 0; w < kRedThreads / 32; ++w) {
-      bd += sd[w];
-      bs += ss[w];
+  auto block_sum = [&](double& a, double& b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xFFFFFFFFu, a, off);
+      b += __shfl_xor_sync(0xFFFFFFFFu, b, off);
     }
-    partial[2 * blockIdx.x] = bd;
-    partial[2 * blockIdx.x + 1] = bs;
+    if (lane == 0) {
+      sd[warp] = a;
+      ss[warp] = b;
+    }
+    __syncthreads();
+    a = 0.0;
+    b = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) {
+      a += sd[w];
+      b += ss[w];
+    }
+  };
+  block_sum(d, s);
+  if (threadIdx.x == 0) {
+    sc->partial[2 * blockIdx.x] = d;
+    sc->partial[2 * blockIdx.x + 1] = s;
     __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
   double td = 0.0, ts = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
-    td += __ldcg(partial + 2 * b);
-    ts += __ldcg(partial + 2 * b + 1);
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    td += __ldcg(sc->partial + 2 * b);
+    ts += __ldcg(sc->partial + 2 * b + 1);
   }
-  if (MODE & 4) out[0] = td;
-  if (MODE & 1) out[1] = ts;
-  *ticket = 0;  // ready for the next launch (stream order)
+  __syncthreads();  // sd / ss reuse
+  block_sum(td, ts);
+  if (threadIdx.x == 0) {
+    double* out = iter_out(sc, norms);
+    if (MODE & 4) out[0] = td;
+    if (MODE & 1) out[1] = ts;
+    sc->ticket = 0;  // ready for the next reduction (stream order)
+    if (MODE & 8) sc->iter += 1;
+  }
 }
 
 template <int MODE>
-void launch_reduce(const double* x, double* y, uint64_t n, const double* mass_in, double* partial, unsigned* ticket,
-                   double* out, cudaStream_t s) {
-  const unsigned grid = (unsigned)std::min<uint64_t>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads);
-  iter_reduce_kernel<MODE><<<grid ? grid : 1, kRedThreads, 0, s>>>(x, y, n, mass_in, partial, ticket, out);
+void launch_reduce(const double* x, double* y, uint64_t n, IterScratch* sc, double* norms, cudaStream_t s) {
+  const uint64_t want = (n + (uint64_t)kRedThreads * kRedUnroll - 1) / ((uint64_t)kRedThreads * kRedUnroll);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks, want));
+  iter_reduce_kernel<MODE><<<grid, kRedThreads, 0, s>>>(x, y, n, sc, norms);
   note_launch();
+}
+
+int one_iteration(const SpmvFn& multiply, const double* cur, double* nxt, uint64_t n, bool normalize, double* norms,
+                  IterScratch* sc, cudaStream_t s) {
+  if (int rc = multiply(cur, nxt, s)) return rc;
+  if (normalize) {
+    launch_reduce<1>(cur, nxt, n, sc, norms, s);          // mass of A x_k
+    launch_reduce<2 | 4 | 8>(cur, nxt, n, sc, norms, s);  // rescale, then |x_{k+1} - x_k|
+  } else if (norms) {
+    launch_reduce<1 | 4 | 8>(cur, nxt, n, sc, norms, s);
+  }
+  return kOk;
 }
 
 }  // namespace
@@ -91,36 +148,47 @@ void launch_reduce(const double* x, double* y, uint64_t n, const double* mass_in
 int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
             double* norms, cudaStream_t s) {
   const uint64_t n = f.n;
-  const bool normalize = flags & 1;
-  // scratch: per-CTA partials, the ticket, and a (diff, mass) pair when the caller keeps no norms
-  double* partial = nullptr;
-  if (cudaMallocAsync(&partial, sizeof(double) * (2 * kRedBlocks + 2) + 64, s) != cudaSuccess) {
+  const bool normalize = flags & 1, graph = flags & 2;
+  IterScratch* sc = nullptr;
+  if (cudaMallocAsync(&sc, sizeof(IterScratch), s) != cudaSuccess) {
     cudaGetLastError();
     g_last_error = "device allocation failed (iterate scratch)";
     return kNoMemory;
   }
-  double* pair = partial + 2 * kRedBlocks;
-  unsigned* ticket = reinterpret_cast<unsigned*>(pair + 2);
-  cudaMemsetAsync(ticket, 0, sizeof(unsigned), s);
+  cudaMemsetAsync(sc, 0, sizeof(IterScratch), s);
+  int rc = kOk;
+  uint32_t done = 0;
+  if (graph && iters >= 2) {
+    // capture one (x -> work -> x) pair and replay it; the suspended instrumentation brackets and
+    // the per-stream scratch were settled by the caller
+    cudaGraph_t g = nullptr;
+    const uint64_t l0 = spmvlab_cuda_launch_count();
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      rc = check_launch("iterate(capture)");
+    } else {
+      rc = one_iteration(multiply, x, work, n, normalize, norms, sc, s);
+      if (rc == kOk) rc = one_iteration(multiply, work, x, n, normalize, norms, sc, s);
+      const cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (rc == kOk && ce != cudaSuccess) rc = check_launch("iterate(capture)");
+    }
+    cudaGraphExec_t ge = nullptr;
+    if (rc == kOk && cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) rc = check_launch("iterate(instantiate)");
+    const uint64_t per_pair = spmvlab_cuda_launch_count() - l0;  // kernels in one captured pair
+    for (; rc == kOk && done + 2 <= iters; done += 2) {
+      if (cudaGraphLaunch(ge, s) != cudaSuccess) rc = check_launch("iterate(launch)");
+      if (done) note_launch((unsigned)per_pair);  // the capture counted the first replay
+    }
+    if (ge) cudaGraphExecDestroy(ge);  // freed once in-flight launches complete
+    if (g) cudaGraphDestroy(g);
+  }
   double* cur = x;
   double* nxt = work;
-  int rc = kOk;
-  for (uint32_t k = 0; k < iters && rc == kOk; ++k) {
-    rc = multiply(cur, nxt, s);
-    if (rc) break;
-    double* out = norms ? norms + 2 * k : pair;
-    if (normalize) {
-      launch_reduce<1>(cur, nxt, n, nullptr, partial, ticket, out, s);     // mass of A x_k
-      launch_reduce<2 | 4>(cur, nxt, n, out + 1, partial, ticket, out, s);  // rescale, then |diff|
-    } else if (norms) {
-      launch_reduce<1 | 4>(cur, nxt, n, nullptr, partial, ticket, out, s);
-    }
+  for (; rc == kOk && done < iters; ++done) {
+    rc = one_iteration(multiply, cur, nxt, n, normalize, norms, sc, s);
     std::swap(cur, nxt);
   }
-  if (rc == kOk && cur != x && n) {
-    cudaMemcpyAsync(x, cur, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
-  }
-  cudaFreeAsync(partial, s);
+  if (rc == kOk && cur != x && n) cudaMemcpyAsync(x, cur, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+  cudaFreeAsync(sc, s);
   return rc ? rc : check_launch("iterate");
 }
 
