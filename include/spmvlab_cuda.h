@@ -143,6 +143,45 @@ int spmvlab_cuda_cache_write(const char* path, const spmvlab_cuda_coo* a, void* 
 /* Releases the arrays of a triplet returned by spmvlab_cuda_cache_read. */
 void spmvlab_cuda_free_coo(spmvlab_cuda_coo* a);
 
+/* --- Matrix Market coordinate text (inc/matrix_market.hpp:94-190) ------------------------------ */
+
+/* MatrixHeader (inc/matrix_market.hpp:35-41): field 0 real, 1 integer, 2 pattern; symmetry
+ * 0 general, 1 symmetric; declared_nnz = the size line's entry count (before mirroring). */
+typedef struct {
+  int field;
+  int symmetry;
+  uint32_t m, n;
+  uint64_t declared_nnz;
+} spmvlab_cuda_mm_header;
+
+/* A triplet in HOST memory (malloc'd by the library; release with spmvlab_cuda_free_host_coo). */
+typedef struct {
+  uint32_t m;
+  uint32_t n;
+  uint64_t nnz;
+  uint32_t* row_ind;
+  uint32_t* col_ind;
+  double* data;
+} spmvlab_cuda_host_coo;
+
+/* read_matrix_market (inc/matrix_market.hpp:94-190): banner checks, 1-based -> 0-based, symmetric
+ * off-diagonals mirrored right after their entry, pattern -> 1.0, then validate() -- into device
+ * buffers (caller-owned with capacity a->nnz, or library-allocated when a's pointers are NULL:
+ * release with spmvlab_cuda_free_coo).  header may be NULL.  Errors: BadHeader, UnsupportedFormat,
+ * UnsupportedField, UnsupportedSymmetry, Truncated, ParseError, Overflow, IndexOutOfRange,
+ * DuplicateEntry, IoError. */
+int spmvlab_cuda_read_matrix_market(const char* path, spmvlab_cuda_coo* a, spmvlab_cuda_mm_header* header,
+                                    void* stream);
+
+/* The same parse + validate entirely on the host (no CUDA calls). */
+int spmvlab_cuda_read_matrix_market_host(const char* path, spmvlab_cuda_host_coo* out,
+                                         spmvlab_cuda_mm_header* header);
+void spmvlab_cuda_free_host_coo(spmvlab_cuda_host_coo* a);
+
+/* load_matrix (inc/io.hpp:29-40): SPMVLAB1 cache if the file starts with the magic, else Matrix
+ * Market text; device buffers as in spmvlab_cuda_cache_read. */
+int spmvlab_cuda_load_matrix(const char* path, spmvlab_cuda_coo* a, void* stream);
+
 /* --- primitives, exposed for parity tests ---------------------------------------------------- */
 
 /* select_block_size -- inc/block_size.hpp:47-61 (value_size 8). Host computation. */

@@ -6,6 +6,7 @@ host mirror of the reference's algorithm interface (inc/engine.hpp).
 from .engine import (  # noqa: F401
     Algorithm, BuiltFormat, EngineOptions, Error, ErrorKind, StorageBreakdown, TripletMatrix,
     algorithm_from_name, algorithm_name, all_algorithms, build_format, cache_read, cache_write, curve_keys,
+    MatrixHeader, load_matrix, read_matrix_market, read_matrix_market_host,
     engine_block_size, exclusive_scan, iterate, merge_path_search, partition_rows_by_nnz, run_spmv,
     run_spmv_host, select_block_size, sort_pairs, storage_report, validate,
 )

@@ -22,8 +22,19 @@ EXPORTS = [
     "spmvlab_cuda_curve_keys", "spmvlab_cuda_sort_pairs", "spmvlab_cuda_exclusive_scan",
     "spmvlab_cuda_launch_count", "spmvlab_cuda_kernel_timing", "spmvlab_cuda_kernel_time",
     "spmvlab_cuda_cache_read", "spmvlab_cuda_cache_write", "spmvlab_cuda_free_coo", "spmvlab_cuda_cache_info",
-    "spmvlab_cuda_iterate",
+    "spmvlab_cuda_iterate", "spmvlab_cuda_read_matrix_market", "spmvlab_cuda_read_matrix_market_host",
+    "spmvlab_cuda_free_host_coo", "spmvlab_cuda_load_matrix",
 ]
+
+
+class MmHeader(C.Structure):
+    _fields_ = [("field", C.c_int), ("symmetry", C.c_int), ("m", C.c_uint32), ("n", C.c_uint32),
+                ("declared_nnz", C.c_uint64)]
+
+
+class HostCoo(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("n", C.c_uint32), ("nnz", C.c_uint64), ("row_ind", C.POINTER(C.c_uint32)),
+                ("col_ind", C.POINTER(C.c_uint32)), ("data", C.POINTER(C.c_double))]
 
 
 class Coo(C.Structure):
@@ -64,6 +75,11 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_build_format.argtypes = [i, C.POINTER(Coo), C.c_uint, C.POINTER(Options), C.POINTER(vp), vp]
     L.spmvlab_cuda_run_spmv.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp]
     L.spmvlab_cuda_iterate.argtypes = [i, vp, vp, vp, u32, C.c_uint, i, vp, vp]
+    L.spmvlab_cuda_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(Coo), C.POINTER(MmHeader), vp]
+    L.spmvlab_cuda_read_matrix_market_host.argtypes = [C.c_char_p, C.POINTER(HostCoo), C.POINTER(MmHeader)]
+    L.spmvlab_cuda_free_host_coo.argtypes = [C.POINTER(HostCoo)]
+    L.spmvlab_cuda_free_host_coo.restype = None
+    L.spmvlab_cuda_load_matrix.argtypes = [C.c_char_p, C.POINTER(Coo), vp]
     L.spmvlab_cuda_run_spmv_host.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp, vp, vp]
     L.spmvlab_cuda_storage_report.argtypes = [vp, C.POINTER(StorageArray), C.c_size_t, C.POINTER(C.c_size_t)]
     L.spmvlab_cuda_get_format_info.argtypes = [vp, C.POINTER(FormatInfo)]

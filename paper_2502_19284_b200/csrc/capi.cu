@@ -451,6 +451,34 @@ void spmvlab_cuda_free_coo(spmvlab_cuda_coo* a) {
   std::memset(a, 0, sizeof(*a));
 }
 
+int spmvlab_cuda_read_matrix_market(const char* path, spmvlab_cuda_coo* a, spmvlab_cuda_mm_header* header,
+                                    void* stream) {
+  if (!path || !a) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return mm_read_device(path, a, header, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_read_matrix_market_host(const char* path, spmvlab_cuda_host_coo* out,
+                                         spmvlab_cuda_mm_header* header) {
+  if (!path || !out) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return mm_read_host(path, out, header);
+}
+
+void spmvlab_cuda_free_host_coo(spmvlab_cuda_host_coo* a) {
+  if (!a) return;
+  std::free(a->row_ind);
+  std::free(a->col_ind);
+  std::free(a->data);
+  std::memset(a, 0, sizeof(*a));
+}
+
+int spmvlab_cuda_load_matrix(const char* path, spmvlab_cuda_coo* a, void* stream) {
+  if (!path || !a) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return load_matrix(path, a, static_cast<cudaStream_t>(stream));
+}
+
 uint64_t spmvlab_cuda_launch_count(void) { return g_launches.load(); }
 
 void spmvlab_cuda_kernel_timing(int enable) {

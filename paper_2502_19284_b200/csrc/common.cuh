@@ -14,8 +14,13 @@ enum Status : int {
   kInvalidArgument = 2,
   kCorruptFormat = 3,
   kOverflow = 4,
+  kBadHeader = 5,
+  kUnsupportedFormat = 6,
+  kUnsupportedField = 7,
+  kUnsupportedSymmetry = 8,
   kIndexOutOfRange = 9,
   kDuplicateEntry = 10,
+  kParseError = 11,
   kTruncated = 12,
   kBadMagic = 13,
   kIoError = 14,

@@ -54,6 +54,9 @@ int validate_coo(const spmvlab_cuda_coo& a, Arena& ar);
 int cache_read(const char* path, spmvlab_cuda_coo* a, cudaStream_t s);
 int cache_info(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz);
 int cache_write(const char* path, const spmvlab_cuda_coo& a, cudaStream_t s);
+int mm_read_host(const char* path, spmvlab_cuda_host_coo* out, spmvlab_cuda_mm_header* header);
+int mm_read_device(const char* path, spmvlab_cuda_coo* a, spmvlab_cuda_mm_header* header, cudaStream_t s);
+int load_matrix(const char* path, spmvlab_cuda_coo* a, cudaStream_t s);
 
 // ---- instrumentation: launch counter and dominant-kernel event brackets (capi.cu)
 void note_launch(unsigned n = 1);

@@ -312,6 +312,87 @@ def cache_read(path: str, stream=None) -> TripletMatrix:
     return TripletMatrix(int(coo.m), int(coo.n), rows[:k], cols[:k], vals[:k])
 
 
+@dataclass
+class MatrixHeader:
+    """MatrixHeader (inc/matrix_market.hpp:35-41)."""
+    field: str      # "real" | "integer" | "pattern"
+    symmetry: str   # "general" | "symmetric"
+    m: int
+    n: int
+    declared_nnz: int
+
+
+def _mm_header(h) -> MatrixHeader:
+    return MatrixHeader(("real", "integer", "pattern")[h.field], ("general", "symmetric")[h.symmetry], int(h.m),
+                        int(h.n), int(h.declared_nnz))
+
+
+def _device_coo_to_triplet(coo) -> TripletMatrix:
+    """Copies a library-allocated device triplet into torch tensors and releases it."""
+    L = capi.load()
+    k = int(coo.nnz)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rows = torch.empty(k, dtype=torch.int32, device=dev)
+    cols = torch.empty(k, dtype=torch.int32, device=dev)
+    vals = torch.empty(k, dtype=torch.float64, device=dev)
+    class _View:  # __cuda_array_interface__ view of library memory, copied before it is released
+        def __init__(self, ptr, typestr):
+            self.__cuda_array_interface__ = {"shape": (k,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                             "strides": None}
+
+    try:
+        if k:
+            rows.copy_(torch.as_tensor(_View(coo.row_ind, "<i4"), device=dev))
+            cols.copy_(torch.as_tensor(_View(coo.col_ind, "<i4"), device=dev))
+            vals.copy_(torch.as_tensor(_View(coo.data, "<f8"), device=dev))
+            torch.cuda.synchronize()
+    finally:
+        L.spmvlab_cuda_free_coo(C.byref(coo))
+    return TripletMatrix(int(coo.m), int(coo.n), rows, cols, vals)
+
+
+def read_matrix_market(path: str, stream=None, with_header: bool = False):
+    """read_matrix_market (inc/matrix_market.hpp:94-190) into a device triplet (validated on the
+    device).  Returns the TripletMatrix, or (TripletMatrix, MatrixHeader) with with_header."""
+    L = capi.load()
+    coo = capi.Coo(0, 0, 0, None, None, None)
+    h = capi.MmHeader()
+    _check(L.spmvlab_cuda_read_matrix_market(str(path).encode(), C.byref(coo), C.byref(h), _stream(stream)))
+    torch.cuda.synchronize()
+    m, n = int(coo.m), int(coo.n)
+    a = _device_coo_to_triplet(coo)
+    a.m, a.n = m, n
+    return (a, _mm_header(h)) if with_header else a
+
+
+def read_matrix_market_host(path: str):
+    """The same parse + validate on the host: (m, n, rows u32, cols u32, vals f64, MatrixHeader)."""
+    L = capi.load()
+    out = capi.HostCoo()
+    h = capi.MmHeader()
+    _check(L.spmvlab_cuda_read_matrix_market_host(str(path).encode(), C.byref(out), C.byref(h)))
+    try:
+        k = int(out.nnz)
+        rows = np.ctypeslib.as_array(out.row_ind, shape=(k,)).copy() if k else np.zeros(0, np.uint32)
+        cols = np.ctypeslib.as_array(out.col_ind, shape=(k,)).copy() if k else np.zeros(0, np.uint32)
+        vals = np.ctypeslib.as_array(out.data, shape=(k,)).copy() if k else np.zeros(0, np.float64)
+        return int(out.m), int(out.n), rows, cols, vals, _mm_header(h)
+    finally:
+        L.spmvlab_cuda_free_host_coo(C.byref(out))
+
+
+def load_matrix(path: str, stream=None) -> TripletMatrix:
+    """load_matrix (inc/io.hpp:29-40): SPMVLAB1 cache or Matrix Market text, sniffed by magic."""
+    L = capi.load()
+    coo = capi.Coo(0, 0, 0, None, None, None)
+    _check(L.spmvlab_cuda_load_matrix(str(path).encode(), C.byref(coo), _stream(stream)))
+    torch.cuda.synchronize()
+    m, n = int(coo.m), int(coo.n)
+    a = _device_coo_to_triplet(coo)
+    a.m, a.n = m, n
+    return a
+
+
 def cache_write(path: str, a: TripletMatrix, stream=None) -> None:
     """Device triplet -> SPMVLAB1 cache, byte-identical to the reference's cache_write."""
     coo = a._c()
