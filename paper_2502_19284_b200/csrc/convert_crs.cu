@@ -139,6 +139,10 @@ int build_merge_plan(Format& f, Arena& ar) {
   cudaStream_t s = ar.stream();
   const uint64_t total = (uint64_t)f.m + f.nnz;
   int th = kMergeThreads, ipt = kMergeIpt, var = kMergeVariant;
+  // tile size: the largest of 32 / 16 / 8 items per lane that still leaves >= 4 warp tiles per
+  // resident warp slot (148 SMs x 48 warps), so small matrices keep every SM busy
+  const uint64_t slots = 4ull * kNumSMs * 48;
+  ipt = total >= slots * 32 * 32 ? 32 : (total >= slots * 32 * 16 ? 16 : 8);
   if (const char* e = getenv("SPMVLAB_MERGE_CFG")) {  // developer override "threads,ipt,variant"
     int a = 0, b = 0, c = 0;
     if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && merge_shape_supported(a, b, c)) {

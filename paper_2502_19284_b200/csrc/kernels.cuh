@@ -18,9 +18,10 @@ constexpr int kVariantSmem = 0;
 constexpr int kVariantTma = 1;
 constexpr int kVariantShuffle = 2;
 constexpr int kVariantWarpStage = 3;
+constexpr int kVariantVector = 4;
 constexpr int kMergeThreads = 256;
-constexpr int kMergeIpt = 7;
-constexpr int kMergeVariant = kVariantWarpStage;
+constexpr int kMergeIpt = 32;  // upper bound; build_merge_plan picks 32 / 16 / 8 by matrix size
+constexpr int kMergeVariant = kVariantVector;
 // ParCRS: rows longer than kParLongIters * group width are summed by a whole CTA (a sub-warp group
 // would walk them serially -- R-MAT s22 row 0 has ~10^5 nonzeros); those CTAs come first in the grid.
 constexpr uint32_t kParLongIters = 32;

@@ -9,8 +9,14 @@
 //    0..nnz-1) is cut into equal tiles at build time (merge_partition: one diagonal search per
 //    tile boundary, spmv_parallel.hpp:47-86).  Each tile leaves one (row, partial) carry-out and a
 //    fix-up kernel adds the carries of rows spanning tiles in tile order (deterministic; the
-//    sequential carry loop of spmv_parallel.hpp:157-159).  Four tile kernels:
-//      - kVariantWarpStage (default, 256 x 7): one tile of 32*IPT items per WARP in warp-private
+//    sequential carry loop of spmv_parallel.hpp:157-159).  Five tile kernels:
+//      - kVariantVector (default, 256 threads, 32 * {32,16,8} items per warp tile by matrix size):
+//        the tile's nonzeros in lane-blocked passes of 128 -- each lane loads 4 consecutive
+//        col_ind / data entries with one 128-bit and one 256-bit load, gathers and multiplies in
+//        registers (two passes in flight); row ends of the pass are scattered to the element they
+//        close through a 128-entry shared map, each lane walks its 4 products, one warp segmented
+//        scan joins the lanes.  No product staging.  cfg2: 297 us.
+//      - kVariantWarpStage (256 x 7): one tile of 32*IPT items per WARP in warp-private
 //        shared memory, warp synchronisation only: coalesced streaming loads of row ends /
 //        col_ind / data (all IPT in flight per lane), IPT x gathers in flight, products staged,
 //        lane start points by scattering row ends to their owners + shuffle suffix-minimum,
@@ -507,6 +513,129 @@ __global__ void __launch_bounds__(WARPS * 32, (IPT <= 7 ? 48 : 32) / WARPS) merg
   }
 }
 
+// ---------------------------------------------------------------- lane-blocked vector variant
+
+// 4 consecutive nonzeros of a 128-element pass per lane, loaded with one 128-bit col_ind load and
+// one 256-bit data load (sm_100 ld.global.v4.f64); the products never leave registers.  Elements
+// outside [j0, j1) are masked (the tile's merge-path element range is not 4-aligned).
+__device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, const double* __restrict__ val,
+                                             const double* __restrict__ x, uint32_t k, uint32_t j0, uint32_t j1,
+                                             uint64_t pf, uint64_t pl, double p[4]) {
+  if (k >= j0 && k + 3 < j1) {
+    const uint4 c = ld_stream4(col + k, pf);
+    double v0, v1, v2, v3;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
+    p[0] = v0 * ld_x(x + c.x, pl);
+    p[1] = v1 * ld_x(x + c.y, pl);
+    p[2] = v2 * ld_x(x + c.z, pl);
+    p[3] = v3 * ld_x(x + c.w, pl);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t e = k + u;
+      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * ld_x(x + ld_stream(col + e, pf), pl) : 0.0;
+    }
+  }
+}
+
+// One 128-element pass of a warp tile.  Row ends falling in the pass are read 32 at a time from
+// row_ptr and scattered to the element they close (smap: element -> row, -1 = none); each lane
+// then walks its 4 products in registers, stores rows that close inside the lane, and the lane
+// tails are combined by one warp segmented scan (carry = the open row's running sum).
+__device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, double* __restrict__ y, int* smap,
+                                         uint32_t base, uint32_t j0, uint32_t j1, uint32_t r1, uint32_t& rp,
+                                         uint32_t& prevE, const double p[4], double& carry, unsigned lane) {
+  const uint32_t pend = min(base + 128u, j1);
+  while (rp < r1) {
+    const uint32_t idx = rp + lane;
+    const bool have = idx < r1;
+    const uint32_t E = have ? __ldg(row_ptr + idx + 1) : 0xFFFFFFFFu;
+    uint32_t S = __shfl_up_sync(0xFFFFFFFFu, E, 1);
+    if (lane == 0) S = prevE;
+    const bool in = have && E <= pend;
+    if (in) {
+      if (E == S || E <= j0) y[idx] = 0.0;  // empty row, or a row whose elements precede the tile
+      else smap[E - 1 - base] = (int)idx;   // closes at element E - 1 of this pass
+    }
+    const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
+    const int nin = __popc(inmask);
+    if (nin) prevE = __shfl_sync(0xFFFFFFFFu, E, nin - 1);
+    rp += (uint32_t)nin;
+    if (nin < 32) break;
+  }
+  __syncwarp();
+  int4 m4 = *reinterpret_cast<int4*>(smap + 4 * lane);
+  *reinterpret_cast<int4*>(smap + 4 * lane) = make_int4(-1, -1, -1, -1);
+  const int rid[4] = {m4.x, m4.y, m4.z, m4.w};
+  double run = 0.0, first_val = 0.0;
+  int first_row = -1;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    run += p[u];
+    if (rid[u] >= 0) {
+      if (first_row < 0) {
+        first_row = rid[u];
+        first_val = run;
+      } else {
+        y[rid[u]] = run;
+      }
+      run = 0.0;
+    }
+  }
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, first_row >= 0);
+  const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int seg = heads & le ? 31 - __clz(heads & le) : 0;
+  double v = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ov = __shfl_up_sync(0xFFFFFFFFu, v, off);
+    if ((int)lane - off >= seg) v += ov;
+  }
+  double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+  if (lane == 0) ex = 0.0;
+  if (first_row >= 0) y[first_row] = first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry);
+  const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
+  carry = heads ? v31 : carry + v31;
+  __syncwarp();
+}
+
+// Merge-path tiles of 32 * IPT items per warp (the same partition and carry fix-up as the other
+// variants), the tile's elements walked in lane-blocked passes of 128 with two passes' loads and
+// gathers in flight.  No product staging: shared memory holds only the 128-entry row map.
+template <int IPT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
+    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+    double* __restrict__ carry_val, uint32_t tiles) {
+  __shared__ __align__(16) int s_map_all[WARPS][128];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x * WARPS + warp;
+  if (t >= tiles) return;
+  int* smap = s_map_all[warp];
+  *reinterpret_cast<int4*>(smap + 4 * lane) = make_int4(-1, -1, -1, -1);
+  const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+  const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  uint32_t rp = r0;
+  uint32_t prevE = __ldg(row_ptr + r0);
+  double carry = 0.0;
+  for (uint32_t base = j0 & ~3u;; base += 256u) {
+    double pa[4], pb[4];
+    vec_products(col, val, x, base + 4 * lane, j0, j1, pf, pl, pa);
+    vec_products(col, val, x, base + 128u + 4 * lane, j0, j1, pf, pl, pb);
+    vec_pass(row_ptr, y, smap, base, j0, j1, r1, rp, prevE, pa, carry, lane);
+    if (!(base + 128u < j1 || rp < r1)) break;
+    vec_pass(row_ptr, y, smap, base + 128u, j0, j1, r1, rp, prevE, pb, carry, lane);
+    if (!(base + 256u < j1 || rp < r1)) break;
+  }
+  if (lane == 0) {
+    carry_row[t] = r1;
+    carry_val[t] = carry;
+  }
+}
+
 // ---------------------------------------------------------------- TMA variant
 
 template <int THREADS, int IPT, int STAGES>
@@ -671,6 +800,13 @@ void launch_merge_wstage(const Format& f, const double* x, double* y, const Scra
 }
 
 template <int THREADS, int IPT>
+void launch_merge_vec(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
+  constexpr int WARPS = THREADS / 32;
+  merge_spmv_vec_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
+                                                                                            f.merge_tiles);
+}
+
+template <int THREADS, int IPT>
 void launch_merge_smem(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   merge_spmv_smem_kernel<THREADS, IPT><<<f.merge_tiles, THREADS, 0, s>>>(MERGE_ARGS);
 }
@@ -739,17 +875,27 @@ bool merge_shape_supported(int threads, int ipt, int variant) {
 }
 
 uint32_t merge_tile_items(int threads, int ipt, int variant) {
-  const bool per_warp = variant == kVariantShuffle || variant == kVariantWarpStage;
+  const bool per_warp = variant == kVariantShuffle || variant == kVariantWarpStage || variant == kVariantVector;
   return (uint32_t)((per_warp ? 32 : threads) * ipt);
 }
 
 static const char* merge_kernel_name(int variant) {
   switch (variant) {
+    case kVariantVector: return "merge_spmv_vec_kernel";
     case kVariantShuffle: return "merge_spmv_shfl_kernel";
     case kVariantWarpStage: return "merge_spmv_wstage_kernel";
     case kVariantTma: return "merge_spmv_tma_kernel";
     default: return "merge_spmv_smem_kernel";
   }
+}
+
+template <int T, int I, int V>
+static void launch_merge_shape(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
+  if constexpr (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);
+  else if constexpr (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s);
+  else if constexpr (V == kVariantVector) launch_merge_vec<T, I>(f, x, y, sc, s);
+  else if constexpr (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s);
+  else launch_merge_tma<T, I, 2>(f, x, y, sc, s);
 }
 
 int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
@@ -762,13 +908,10 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   }
   bool launched = false;
   timing_begin(merge_kernel_name(variant), s);
-#define SPMV_MERGE_SHAPE(T, I, V)                                    \
-  if (!launched && threads == T && ipt == I && variant == V) {       \
-    if (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);   \
-    else if (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s); \
-    else if (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s); \
-    else launch_merge_tma<T, I, 2>(f, x, y, sc, s);                      \
-    launched = true;                                                     \
+#define SPMV_MERGE_SHAPE(T, I, V)                              \
+  if (!launched && threads == T && ipt == I && variant == V) { \
+    launch_merge_shape<T, I, V>(f, x, y, sc, s);               \
+    launched = true;                                           \
   }
 #include "merge_shapes.inc"
 #undef SPMV_MERGE_SHAPE

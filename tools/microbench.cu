@@ -172,3 +172,42 @@ int mb_gather_mul(const uint32_t* col, const double* val, uint64_t nnz, const do
   return (int)cudaGetLastError();
 }
 }
+
+// blocked: lane l of a warp handles 4 consecutive elements of each 128-element group (one 128-bit
+// col load + one 256-bit val load per lane), gathers in lane-blocked order
+template <int Q>
+__global__ void gather_mul_blocked4(const uint32_t* __restrict__ col, const double* __restrict__ val, uint64_t nnz,
+                                    const double* __restrict__ x, double* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0;
+  for (uint64_t g = warp * Q; g * 128 < nnz; g += nwarps * Q) {
+    uint4 c[Q];
+    double v[Q][4];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint64_t k = (g + q) * 128 + 4 * lane;
+      if (k + 3 < nnz) {
+        c[q] = __ldg(reinterpret_cast<const uint4*>(col + k));
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(v[q][0]), "=d"(v[q][1]), "=d"(v[q][2]), "=d"(v[q][3]) : "l"(val + k));
+      } else {
+        c[q] = make_uint4(0, 0, 0, 0);
+        v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      acc += v[q][0] * __ldg(x + c[q].x) + v[q][1] * __ldg(x + c[q].y) + v[q][2] * __ldg(x + c[q].z) +
+             v[q][3] * __ldg(x + c[q].w);
+  }
+  if (acc == 1234.5) out[0] = acc;
+}
+
+extern "C" int mb_gather_mul_blocked4(const uint32_t* col, const double* val, uint64_t nnz, const double* x,
+                                      double* out, int blocks, int q, void* s) {
+  if (q == 1) gather_mul_blocked4<1><<<blocks, 256, 0, (cudaStream_t)s>>>(col, val, nnz, x, out);
+  else gather_mul_blocked4<2><<<blocks, 256, 0, (cudaStream_t)s>>>(col, val, nnz, x, out);
+  return (int)cudaGetLastError();
+}

@@ -80,3 +80,11 @@ L.mb_gather_mul_warp_stage.restype = C.c_int
 L.mb_gather_mul_warp_stage.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
 ms = timeit(lambda: L.mb_gather_mul_warp_stage(colp, valp, nnz, x.data_ptr(), out.data_ptr(), s))
 print(f"gather*val warp-private smem staging (syncwarp): {ms*1e3:.1f} us", flush=True)
+L.mb_gather_mul_blocked4.restype = C.c_int
+L.mb_gather_mul_blocked4.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                     C.c_void_p]
+for q in (1, 2):
+    for blocks in (148 * 8, 148 * 16):
+        ms = timeit(lambda: L.mb_gather_mul_blocked4(colp, valp, nnz, x.data_ptr(), out.data_ptr(), blocks, q, s))
+        print(f"gather*val lane-blocked (4 consecutive per lane, 128/256-bit loads) q={q} blocks={blocks}: "
+              f"{ms*1e3:.1f} us", flush=True)
