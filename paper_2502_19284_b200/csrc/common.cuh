@@ -146,6 +146,79 @@ __host__ __device__ __forceinline__ void hilbert_decode(uint64_t d, unsigned lev
   col = c;
 }
 
+// Table-driven Hilbert coding, 4 bits of row and column per step: enc[state << 8 | r4 << 4 | c4] =
+// (8 output bits | next state << 8), dec[state << 8 | 4 digits] = (r4 | c4 << 4 | next << 8).
+// The tables are the 1-bit automaton above composed four times; a CTA builds them in shared memory
+// (hil_tables_init, then __syncthreads) -- 6 table steps instead of 22-26 automaton steps.
+__device__ __forceinline__ void hil_tables_init(uint16_t* enc, uint16_t* dec) {
+  for (unsigned i = threadIdx.x; i < 1024; i += blockDim.x) {
+    const unsigned st0 = i >> 8, v = i & 255u;
+    unsigned st = st0, out = 0;
+    for (int b = 3; b >= 0; --b) {
+      const unsigned pos = hil_position(st, (v >> (4 + b)) & 1u, (v >> b) & 1u);
+      out = (out << 2) | pos;
+      st = hil_child(st, pos);
+    }
+    enc[i] = (uint16_t)(out | (st << 8));
+    st = st0;
+    unsigned r = 0, c = 0;
+    for (int b = 3; b >= 0; --b) {
+      const unsigned pos = (v >> (2 * b)) & 3u;
+      unsigned rb, cb;
+      hil_cell(st, pos, rb, cb);
+      r |= rb << b;
+      c |= cb << b;
+      st = hil_child(st, pos);
+    }
+    dec[i] = (uint16_t)(r | (c << 4) | (st << 8));
+  }
+}
+__device__ __forceinline__ uint64_t hilbert_encode_t(uint32_t row, uint32_t col, unsigned level,
+                                                     const uint16_t* enc) {
+  unsigned st = 0;
+  uint64_t v = 0;
+  int b = (int)level - 1;
+  for (; b >= 0 && ((b + 1) & 3); --b) {  // leading level % 4 bits one at a time
+    const unsigned pos = hil_position(st, (row >> b) & 1u, (col >> b) & 1u);
+    v = (v << 2) | pos;
+    st = hil_child(st, pos);
+  }
+  for (; b >= 3; b -= 4) {
+    const unsigned e = enc[(st << 8) | (((row >> (b - 3)) & 15u) << 4) | ((col >> (b - 3)) & 15u)];
+    v = (v << 8) | (e & 255u);
+    st = e >> 8;
+  }
+  return v;
+}
+__device__ __forceinline__ void hilbert_decode_t(uint64_t d, unsigned level, uint32_t& row, uint32_t& col,
+                                                 const uint16_t* dec) {
+  unsigned st = 0;
+  uint32_t r = 0, c = 0;
+  int b = (int)level - 1;
+  for (; b >= 0 && ((b + 1) & 3); --b) {
+    const unsigned pos = (unsigned)((d >> (2 * b)) & 3u);
+    unsigned rb, cb;
+    hil_cell(st, pos, rb, cb);
+    r |= rb << b;
+    c |= cb << b;
+    st = hil_child(st, pos);
+  }
+  for (; b >= 3; b -= 4) {
+    const unsigned e = dec[(st << 8) | (unsigned)((d >> (2 * (b - 3))) & 255u)];
+    r |= (e & 15u) << (b - 3);
+    c |= ((e >> 4) & 15u) << (b - 3);
+    st = e >> 8;
+  }
+  row = r;
+  col = c;
+}
+
+// Declares and builds the CTA's Hilbert tables (s_henc / s_hdec); must run before any early return.
+#define SPMV_HILBERT_TABLES()                        \
+  __shared__ uint16_t s_henc[1024], s_hdec[1024];    \
+  hil_tables_init(s_henc, s_hdec);                   \
+  __syncthreads()
+
 // morton_encode (curves.hpp:107-117): row bit above column bit, by magic-number spreading.
 __host__ __device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
   uint64_t x = v;

@@ -44,7 +44,8 @@ struct Geom {
 
 __device__ __forceinline__ bool is_bcoh_kind(int k) { return k >= kBcohRow; }
 
-__device__ __forceinline__ uint64_t make_key(const Geom& g, uint32_t r, uint32_t c, uint32_t band) {
+__device__ __forceinline__ uint64_t make_key(const Geom& g, uint32_t r, uint32_t c, uint32_t band,
+                                             const uint16_t* henc) {
   const uint32_t br = r >> g.lb, bc = c >> g.lb, ir = r & g.mask, ic = c & g.mask;
   const unsigned lb2 = 2 * g.lb;
   switch (g.kind) {
@@ -52,14 +53,14 @@ __device__ __forceinline__ uint64_t make_key(const Geom& g, uint32_t r, uint32_t
       return ((uint64_t)br << (g.bcbits + lb2)) | ((uint64_t)bc << lb2) | morton_encode(ir, ic, g.lb);
     case kCsbH:
     case kMbH:
-      return ((uint64_t)br << (g.bcbits + lb2)) | ((uint64_t)bc << lb2) | hilbert_encode(ir, ic, g.lb);
+      return ((uint64_t)br << (g.bcbits + lb2)) | ((uint64_t)bc << lb2) | hilbert_encode_t(ir, ic, g.lb, henc);
     case kMbRow:
       return ((uint64_t)br << (g.bcbits + lb2)) | ((uint64_t)bc << lb2) | ((uint64_t)ir << g.lb) | ic;
     case kBcohRow:
       return ((uint64_t)band << (2 * g.element_level)) |
-             (hilbert_encode(br, bc, g.block_level) << lb2) | ((uint64_t)ir << g.lb) | ic;
+             (hilbert_encode_t(br, bc, g.block_level, henc) << lb2) | ((uint64_t)ir << g.lb) | ic;
     default:  // kBcohH
-      return ((uint64_t)band << (2 * g.element_level)) | hilbert_encode(r, c, g.element_level);
+      return ((uint64_t)band << (2 * g.element_level)) | hilbert_encode_t(r, c, g.element_level, henc);
   }
 }
 
@@ -67,7 +68,7 @@ struct Coords {
   uint32_t br, bc, ir, ic, band;
 };
 
-__device__ __forceinline__ Coords decode_key(const Geom& g, uint64_t key) {
+__device__ __forceinline__ Coords decode_key(const Geom& g, uint64_t key, const uint16_t* hdec) {
   Coords o;
   const unsigned lb2 = 2 * g.lb;
   o.band = 0;
@@ -82,19 +83,19 @@ __device__ __forceinline__ Coords decode_key(const Geom& g, uint64_t key) {
       o.ir = (uint32_t)(rank >> g.lb);
       o.ic = (uint32_t)(rank & g.mask);
     } else {
-      hilbert_decode(rank, g.lb, o.ir, o.ic);
+      hilbert_decode_t(rank, g.lb, o.ir, o.ic, hdec);
     }
   } else {
     const unsigned el2 = 2 * g.element_level;
     o.band = (uint32_t)(el2 >= 64 ? 0 : (key >> el2));
     const uint64_t low = el2 >= 64 ? key : (key & ((1ull << el2) - 1ull));
     if (g.kind == kBcohRow) {
-      hilbert_decode(low >> lb2, g.block_level, o.br, o.bc);
+      hilbert_decode_t(low >> lb2, g.block_level, o.br, o.bc, hdec);
       o.ir = (uint32_t)((low >> g.lb) & g.mask);
       o.ic = (uint32_t)(low & g.mask);
     } else {
       uint32_t r, c;
-      hilbert_decode(low, g.element_level, r, c);
+      hilbert_decode_t(low, g.element_level, r, c, hdec);
       o.br = r >> g.lb;
       o.bc = c >> g.lb;
       o.ir = r & g.mask;
@@ -117,6 +118,7 @@ __global__ void blk_keys(const uint32_t* __restrict__ rows, const uint32_t* __re
                          const double* __restrict__ vals, uint64_t nnz, Geom g,
                          const uint32_t* __restrict__ bounds, uint64_t* __restrict__ keys,
                          uint64_t* __restrict__ payload, uint32_t* err) {
+  SPMV_HILBERT_TABLES();
   extern __shared__ uint32_t s_bounds[];
   const bool bcoh = is_bcoh_kind(g.kind);
   if (bcoh)
@@ -131,7 +133,7 @@ __global__ void blk_keys(const uint32_t* __restrict__ rows, const uint32_t* __re
       payload[k] = 0;
       continue;
     }
-    keys[k] = make_key(g, r, c, bcoh ? band_of(s_bounds, g.p, r) : 0u);
+    keys[k] = make_key(g, r, c, bcoh ? band_of(s_bounds, g.p, r) : 0u, s_henc);
     payload[k] = (uint64_t)__double_as_longlong(vals[k]);
   }
 }
@@ -143,12 +145,13 @@ __global__ void blk_populate(const uint64_t* __restrict__ skeys, const uint64_t*
                              double* __restrict__ data, uint16_t* __restrict__ col_inc,
                              uint32_t* __restrict__ blk_flag, uint32_t* __restrict__ rj_flag,
                              uint32_t* __restrict__ cell_counts, uint32_t* err) {
+  SPMV_HILBERT_TABLES();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t beta = 1u << g.lb;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
     const uint64_t key = skeys[k];
-    const Coords c = decode_key(g, key);
+    const Coords c = decode_key(g, key, s_hdec);
     const bool first = k == 0;
     const uint64_t pkey = first ? 0 : skeys[k - 1];
     if (!first && pkey == key) atomicOr(err, 2u);
@@ -162,7 +165,7 @@ __global__ void blk_populate(const uint64_t* __restrict__ skeys, const uint64_t*
         inc = c.ic;
         rjf = 1;
       } else {
-        const Coords pc = decode_key(g, pkey);
+        const Coords pc = decode_key(g, pkey, s_hdec);
         if (c.ir == pc.ir) {
           inc = c.ic - pc.ic;
           rjf = 0;
@@ -190,12 +193,13 @@ __global__ void blk_table(const uint64_t* __restrict__ skeys, uint64_t nnz, Geom
                           uint32_t* __restrict__ blk_begin, uint2* __restrict__ blk_rc,
                           uint32_t* __restrict__ blk_band, uint32_t* __restrict__ blk_rj,
                           uint16_t* __restrict__ row_jump) {
+  SPMV_HILBERT_TABLES();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
     const bool nb = blk_flag[k] != 0;
     const bool rj = rj_flag && rj_flag[k] != 0;
     if (!nb && !rj) continue;
-    const Coords c = decode_key(g, skeys[k]);
+    const Coords c = decode_key(g, skeys[k], s_hdec);
     if (nb) {
       const uint32_t b = blk_scan[k];
       blk_begin[b] = (uint32_t)k;
@@ -205,7 +209,7 @@ __global__ void blk_table(const uint64_t* __restrict__ skeys, uint64_t nnz, Geom
     }
     if (rj) {
       uint32_t v = c.ir;
-      if (!nb) v = c.ir - decode_key(g, skeys[k - 1]).ir;
+      if (!nb) v = c.ir - decode_key(g, skeys[k - 1], s_hdec).ir;
       row_jump[rj_scan[k]] = (uint16_t)v;
     }
   }
@@ -267,6 +271,7 @@ __global__ void hptr_cell_keys(uint64_t total_cells, unsigned p, const uint64_t*
                                const uint32_t* __restrict__ band_fbr, uint32_t block_cols,
                                unsigned block_level, uint64_t* __restrict__ keys,
                                uint32_t* __restrict__ cell_id) {
+  SPMV_HILBERT_TABLES();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t gidx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gidx < total_cells; gidx += stride) {
     unsigned lo = 0, hi = p;  // band = last b with cell_off[b] <= gidx
@@ -277,7 +282,7 @@ __global__ void hptr_cell_keys(uint64_t total_cells, unsigned p, const uint64_t*
     const uint64_t local = gidx - cell_off[lo];
     const uint32_t br = band_fbr[lo] + (uint32_t)(local / block_cols);
     const uint32_t bc = (uint32_t)(local % block_cols);
-    keys[gidx] = ((uint64_t)lo << (2 * block_level)) | hilbert_encode(br, bc, block_level);
+    keys[gidx] = ((uint64_t)lo << (2 * block_level)) | hilbert_encode_t(br, bc, block_level, s_henc);
     cell_id[gidx] = br * block_cols + bc;
   }
 }
@@ -366,6 +371,7 @@ __global__ void chunk_fill(const uint32_t* __restrict__ blk_begin, uint32_t nblk
                            const uint32_t* __restrict__ rj_flag, const uint32_t* __restrict__ rj_scan,
                            const uint32_t* __restrict__ blk_rj, uint32_t* __restrict__ ch_begin,
                            uint32_t* __restrict__ ch_blk, uint4* __restrict__ ch_state) {
+  SPMV_HILBERT_TABLES();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nblk) return;
   const uint32_t e0 = blk_begin[b], e1 = blk_begin[b + 1];
@@ -377,7 +383,7 @@ __global__ void chunk_fill(const uint32_t* __restrict__ blk_begin, uint32_t nblk
       if (e == e0) {
         ch_state[c] = make_uint4(0u, 0xFFFFFFFFu, 0u, blk_rj[b]);
       } else {
-        const Coords pc = decode_key(g, skeys[e - 1]);
+        const Coords pc = decode_key(g, skeys[e - 1], s_hdec);
         const uint32_t rjpos = rj_scan[e - 1] + rj_flag[e - 1] - 1;
         const uint32_t R = rjpos - blk_rj[b];
         ch_state[c] = make_uint4(pc.ic + (R << g.lb), R, pc.ir, rjpos + 1);

@@ -26,9 +26,10 @@ __global__ void adjacent_dups(const uint64_t* __restrict__ keys, uint64_t nnz, u
 __global__ void curve_keys_kernel(int kind, const uint32_t* __restrict__ rows,
                                   const uint32_t* __restrict__ cols, uint64_t count, unsigned level,
                                   uint64_t* __restrict__ keys) {
+  SPMV_HILBERT_TABLES();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride)
-    keys[k] = kind == 0 ? morton_encode(rows[k], cols[k], level) : hilbert_encode(rows[k], cols[k], level);
+    keys[k] = kind == 0 ? morton_encode(rows[k], cols[k], level) : hilbert_encode_t(rows[k], cols[k], level, s_henc);
 }
 
 }  // namespace
