@@ -168,14 +168,18 @@ const DevArray* spmvlab_cuda_format::find(const std::string& name) const {
   return nullptr;
 }
 
-void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t esz, cudaStream_t) {
+void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t esz, cudaStream_t s) {
   DevArray a;
   a.name = name;
   a.esz = esz;
   a.bytes = count * esz;
   // Padded so 16-byte-aligned bulk (TMA) copies may over-read up to 3 elements past the end.
+  // From the device's stream-ordered pool (kept mapped between builds, so rebuilding a format
+  // does not pay the driver's page mapping again); build_format synchronises its stream before
+  // returning, so the arrays are then usable from any stream.  Released with cudaFree.
   const uint64_t alloc = ((a.bytes + 15) & ~uint64_t(15)) + 64;
-  if (cudaMalloc(&a.ptr, alloc) != cudaSuccess) {
+  pool_init();
+  if (cudaMallocAsync(&a.ptr, alloc, s) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }

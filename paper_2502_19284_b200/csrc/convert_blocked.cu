@@ -372,11 +372,20 @@ __global__ void chunk_fill(const uint32_t* __restrict__ blk_begin, uint32_t nblk
                            const uint32_t* __restrict__ blk_rj, uint32_t* __restrict__ ch_begin,
                            uint32_t* __restrict__ ch_blk, uint4* __restrict__ ch_state) {
   SPMV_HILBERT_TABLES();
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nblk) return;
-  const uint32_t e0 = blk_begin[b], e1 = blk_begin[b + 1];
-  uint32_t c = ch_off[b];
-  for (uint32_t e = e0; e < e1; e += chunk, ++c) {
+  // one thread per chunk (a block of 580k elements has 2k+ chunks): its block by binary search
+  // over the blocks' chunk offsets
+  const uint32_t nchunks = ch_off[nblk];
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  uint32_t lo = 0, hi = nblk - 1;  // last b with ch_off[b] <= c
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (ch_off[mid] <= c) lo = mid; else hi = mid - 1;
+  }
+  const uint32_t b = lo;
+  const uint32_t e0 = blk_begin[b];
+  {
+    const uint32_t e = e0 + (c - ch_off[b]) * chunk;
     ch_begin[c] = e;
     ch_blk[c] = b;
     if (ch_state) {
@@ -520,9 +529,9 @@ static int blocked_common(BlockedBuild& bb, const spmvlab_cuda_coo& a, const uin
   uint4* ch_state = want_icrs ? static_cast<uint4*>(f.add("chunk_state", nchunks, 16, s)) : nullptr;
   if (!ch_begin || !ch_blk || (want_icrs && !ch_state)) return kNoMemory;
   cudaMemcpyAsync(ch_begin + nchunks, &nnz32, 4, cudaMemcpyHostToDevice, s);
-  if (nblk)
-    chunk_fill<<<(nblk + 255) / 256, 256, 0, s>>>(blk_begin, nblk, kChunk, nch, sk, bb.g, bb.rj_flag, bb.rj_scan,
-                                                  blk_rj, ch_begin, ch_blk, ch_state);
+  if (nblk && nchunks)
+    chunk_fill<<<(nchunks + 255) / 256, 256, 0, s>>>(blk_begin, nblk, kChunk, nch, sk, bb.g, bb.rj_flag,
+                                                     bb.rj_scan, blk_rj, ch_begin, ch_blk, ch_state);
   f.work_items = nchunks;
   f.needs_zero_y = true;
   return check_launch("blocked_common");

@@ -24,8 +24,8 @@ int check_launch(const char* what) {
   return kOk;
 }
 
-void* Arena::alloc(size_t bytes) {
-  static const bool pool_ready = [] {
+void pool_init() {
+  static const bool ready = [] {
     // Keep freed scratch in the device's default stream-ordered pool between builds instead of
     // returning it to the driver at every synchronisation (conversions allocate GBs of keys).
     int dev = 0;
@@ -37,7 +37,11 @@ void* Arena::alloc(size_t bytes) {
     }
     return true;
   }();
-  (void)pool_ready;
+  (void)ready;
+}
+
+void* Arena::alloc(size_t bytes) {
+  pool_init();
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
   if (cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s_) != cudaSuccess) return nullptr;
@@ -90,6 +94,36 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint32_t tile, ui
     --t;
   }
   st_relaxed(mine, kFlagPrefix | (excl + count));
+  return excl;
+}
+
+// Warp-parallel look-back (one status word per tile; called by a whole warp): each pass inspects
+// the 32 nearest unresolved predecessors at once and stops at the nearest inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint32_t tile, uint64_t count,
+                                                  unsigned lane) {
+  uint64_t* mine = status + tile;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(mine, kFlagPrefix | count);
+    return 0;
+  }
+  if (lane == 0) st_relaxed(mine, kFlagAgg | count);
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = base - (int64_t)lane;
+    uint64_t v = t >= 0 ? ld_relaxed(status + t) : kFlagPrefix;  // before tile 0: prefix 0
+    while (__any_sync(0xFFFFFFFFu, (v & ~kValMask) == 0))
+      if ((v & ~kValMask) == 0) v = ld_relaxed(status + t);
+    const unsigned pmask = __ballot_sync(0xFFFFFFFFu, (v & ~kValMask) == kFlagPrefix);
+    const int stop = pmask ? __ffs(pmask) - 1 : 31;
+    uint64_t val = (int)lane <= stop ? (v & kValMask) : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, off);
+    excl += val;
+    if (pmask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_relaxed(mine, kFlagPrefix | (excl + count));
   return excl;
 }
 
@@ -373,7 +407,10 @@ __global__ void __launch_bounds__(kThreads) scan_u32(const uint32_t* in, uint32_
     if ((unsigned)w < warp) wpre += s_wsum[w];
     total += s_wsum[w];
   }
-  if (tid == 0) s_excl = lookback(status, tile, 0, 1, total);
+  if (warp == 0) {
+    const uint64_t ex = lookback_warp(status, tile, total, lane);
+    if (lane == 0) s_excl = ex;
+  }
   __syncthreads();
   uint32_t run = (uint32_t)s_excl + wpre + incl - sum;
 #pragma unroll

@@ -12,6 +12,9 @@
 namespace spmvcu {
 
 // Stream-ordered scratch allocations released when the arena dies.
+// Keeps freed device memory in the default stream-ordered pool (release threshold = max).
+void pool_init();
+
 class Arena {
  public:
   explicit Arena(cudaStream_t s) : s_(s) {}
