@@ -237,17 +237,18 @@ __global__ void rs_hist_scan(uint32_t* hist) {
   h[threadIdx.x] = s[threadIdx.x];
 }
 
-// Pairs per thread (IPT): only the keys are live in registers while ranking (values are loaded
-// after the ranks are known), which keeps the kernel small enough for 3+ CTAs per SM.  The tile
-// is staged in shared memory as 32-bit halves (keys lo / hi, values lo [/ hi]) so the random
-// digit-order scatter costs 32-bit bank accesses instead of 64-bit ones.
+// Pairs per thread (IPT): only the keys are live in registers while ranking, which keeps the
+// kernel small enough for 3 CTAs per SM.  The tile's values never pass through registers before
+// the write-out: one thread starts a bulk async copy (cp.async.bulk + mbarrier) of the tile's
+// value range into shared memory as soon as the tile index is known, overlapping the key loads
+// and the ranking; the keys are staged in digit order as 32-bit halves with their 16-bit
+// position in the tile, which the write-out uses to fetch the value.
 template <typename V>
 struct OneSweep {
   static constexpr int IPT = 12;
   static constexpr int TILE = kThreads * IPT;
-  static constexpr int VWORDS = sizeof(V) / 4;
-  static constexpr size_t SMEM = sizeof(uint32_t) * TILE * (2 + VWORDS) + sizeof(uint32_t) * kWarps * 256 +
-                                 sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
+  static constexpr size_t SMEM = sizeof(V) * TILE + sizeof(uint32_t) * TILE * 2 + sizeof(uint16_t) * TILE +
+                                 sizeof(uint32_t) * kWarps * 256 + sizeof(uint32_t) * 256 + sizeof(int64_t) * 256;
 };
 
 template <typename V>
@@ -257,24 +258,42 @@ __global__ void __launch_bounds__(kThreads, 3) rs_onesweep(
     const uint32_t* __restrict__ pass_offset, uint64_t* status, uint32_t* tile_counter) {
   constexpr int kIpt = OneSweep<V>::IPT;
   constexpr int kTile = OneSweep<V>::TILE;
-  constexpr int kVw = OneSweep<V>::VWORDS;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* s_klo = reinterpret_cast<uint32_t*>(smem);
+  extern __shared__ __align__(128) uint8_t smem[];
+  V* s_vorig = reinterpret_cast<V*>(smem);                      // values in input order (bulk copy)
+  uint32_t* s_klo = reinterpret_cast<uint32_t*>(s_vorig + kTile);
   uint32_t* s_khi = s_klo + kTile;
-  uint32_t* s_v = s_khi + kTile;                    // kVw planes of kTile words
-  uint32_t* s_whist = s_v + kVw * kTile;            // [warp][digit]
+  uint16_t* s_pos = reinterpret_cast<uint16_t*>(s_khi + kTile);  // input position of each staged key
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(s_pos + kTile);  // [warp][digit]
   uint32_t* s_local = s_whist + kWarps * 256;       // tile-local exclusive digit offsets
   int64_t* s_gbase = reinterpret_cast<int64_t*>(s_local + 256);
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_wsum[kWarps];
+  __shared__ __align__(8) uint64_t s_bar;
 
   const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(tile_counter, 1u);
+    s_tile = t;
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    const uint64_t b0 = (uint64_t)t * kTile;
+    const uint32_t cnt0 = (n - b0) < (uint64_t)kTile ? (uint32_t)(n - b0) : (uint32_t)kTile;
+    const bool aligned = (reinterpret_cast<uintptr_t>(vin) & 15u) == 0;
+    const uint32_t bytes = aligned ? (cnt0 * (uint32_t)sizeof(V)) & ~15u : 0u;  // 16-B multiple; rest below
+    mbar_arrive_expect_tx(&s_bar, bytes);
+    if (bytes) bulk_g2s(s_vorig, vin + b0, bytes, &s_bar, policy_evict_first());
+  }
   for (int i = tid; i < kWarps * 256; i += kThreads) s_whist[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t base = (uint64_t)tile * kTile;
   const uint64_t wbase = base + (uint64_t)warp * (kIpt * 32);
+  const uint32_t valid_n = (n - base) < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
+  {  // the values the 16-byte bulk copy leaves out (a few trailing ones; all if vin is unaligned)
+    const bool aligned = (reinterpret_cast<uintptr_t>(vin) & 15u) == 0;
+    const uint32_t done = aligned ? (valid_n * (uint32_t)sizeof(V) & ~15u) / (uint32_t)sizeof(V) : 0u;
+    for (uint32_t q = done + tid; q < valid_n; q += kThreads) s_vorig[q] = vin[base + q];
+  }
 
   uint64_t key[kIpt];
   uint32_t rank[kIpt];
@@ -331,37 +350,29 @@ __global__ void __launch_bounds__(kThreads, 3) rs_onesweep(
   st_relaxed(mine, (tile == 0 ? kFlagPrefix : kFlagAgg) | cnt);
   __syncthreads();
 
-  // stage the tile in digit order in shared memory (needs only tile-local offsets); the values
-  // are read here, after ranking
+  // stage the keys in digit order in shared memory (needs only tile-local offsets)
 #pragma unroll
   for (int i = 0; i < kIpt; ++i) {
-    const uint64_t idx = wbase + i * 32 + lane;
-    if (idx < n) {
+    const uint32_t li = warp * (kIpt * 32) + i * 32 + lane;
+    if (base + li < n) {
       const unsigned dd = (unsigned)(key[i] >> shift) & dmask;
       const uint32_t pos = s_whist[warp * 256 + dd] + rank[i];
       s_klo[pos] = (uint32_t)key[i];
       s_khi[pos] = (uint32_t)(key[i] >> 32);
-      const V v = vin[idx];
-      if constexpr (kVw == 2) {
-        s_v[pos] = (uint32_t)(uint64_t)v;
-        s_v[kTile + pos] = (uint32_t)((uint64_t)v >> 32);
-      } else {
-        s_v[pos] = (uint32_t)v;
-      }
+      s_pos[pos] = (uint16_t)li;
     }
   }
   // ... then resolve the global offsets by look-back (overlapping predecessors' progress)
   const uint64_t excl = lookback_published(status, tile, d, 256, cnt);
   s_gbase[d] = (int64_t)pass_offset[d] + (int64_t)excl - (int64_t)local_excl;
   __syncthreads();
-  const uint32_t valid_n = (n - base) < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
+  mbar_wait(&s_bar, 0);  // the tile's values have landed
   for (uint32_t j = tid; j < valid_n; j += kThreads) {
     const uint64_t k = ((uint64_t)s_khi[j] << 32) | s_klo[j];
     const unsigned dd = (unsigned)(k >> shift) & dmask;
     const uint64_t o = (uint64_t)(s_gbase[dd] + (int64_t)j);
     kout[o] = k;
-    if constexpr (kVw == 2) vout[o] = (V)(((uint64_t)s_v[kTile + j] << 32) | s_v[j]);
-    else vout[o] = (V)s_v[j];
+    vout[o] = s_vorig[s_pos[j]];
   }
 }
 
