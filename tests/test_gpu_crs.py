@@ -171,6 +171,24 @@ def test_radix_sort_and_scan(cuda):
         np.testing.assert_array_equal(out, np.concatenate([[0], np.cumsum(cnt)]))
 
 
+def test_radix_sort_unaligned_buffers(cuda):
+    """Caller buffers that are not 16-byte aligned take the scalar histogram / value-copy paths."""
+    sp = cuda
+    rng = np.random.default_rng(8)
+    for n in (5, 3071, 3073, 200001):
+        keys = rng.integers(0, 1 << 40, n + 1, dtype=np.int64)
+        keys[1: n // 4] = keys[n // 2]
+        vals = np.arange(n + 1, dtype=np.int32)
+        kbuf, vbuf = torch.from_numpy(keys.copy()).cuda(), torch.from_numpy(vals.copy()).cuda()
+        kd, vd = kbuf[1:], vbuf[1:]  # 8- and 4-byte offsets from the allocation
+        assert kd.data_ptr() % 16 and vd.data_ptr() % 16
+        sp.sort_pairs(kd, vd, 0, 40)
+        order = np.argsort(keys[1:], kind="stable")
+        np.testing.assert_array_equal(kd.cpu().numpy(), keys[1:][order])
+        np.testing.assert_array_equal(vd.cpu().numpy(), vals[1:][order])
+        assert kbuf[0].item() == keys[0] and vbuf[0].item() == vals[0]
+
+
 def test_concurrent_streams_share_one_format(cuda, oracle):
     """Formats are immutable and shareable (inc/engine.hpp ownership): multiplies of
     one format on several streams at once must not interfere (per-stream carry scratch)."""
