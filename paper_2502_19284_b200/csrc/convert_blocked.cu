@@ -336,6 +336,42 @@ __global__ void band_offsets(const uint64_t* __restrict__ skeys, uint64_t nnz, u
   off_rjb[b] = rjb_scan ? rjb_scan[blo] : 0;
 }
 
+// partition_rows_by_nnz only needs its greedy row rounded to the nearest block-row boundary,
+// cut = (r* + beta/2) >> lb: i.e. which "rounding cell" [c*beta - beta/2, (c+1)*beta - beta/2)
+// holds r*.  Deciding that needs prefix[] only at the rows just before each cell end, so two
+// counters per cell suffice -- the cell total and the count of its last row -- accumulated in
+// shared memory (a few thousand cells) instead of one global atomic per entry into m counters.
+constexpr uint32_t kMaxRoundCells = 6144;
+
+__global__ void round_cell_hist(const uint32_t* __restrict__ rows, uint64_t nnz, uint32_t m, unsigned lb,
+                                uint32_t cells, uint32_t* __restrict__ total, uint32_t* __restrict__ last) {
+  __shared__ uint32_t s_tot[kMaxRoundCells], s_last[kMaxRoundCells];
+  for (uint32_t i = threadIdx.x; i < cells; i += blockDim.x) s_tot[i] = s_last[i] = 0;
+  __syncthreads();
+  const uint32_t half = 1u << (lb - 1), bmask = (1u << lb) - 1u;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = 0; base < nnz; base += stride) {
+    const uint64_t k = base + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = k < nnz;
+    const uint32_t r = valid ? rows[k] : 0u;
+    const bool ok = valid && r < m;
+    const uint32_t c = (uint32_t)(((uint64_t)r + half) >> lb);
+    const uint32_t c0 = __shfl_sync(0xFFFFFFFFu, c, 0);
+    if (__all_sync(0xFFFFFFFFu, ok && c == c0)) {
+      if (lane == 0) atomicAdd(&s_tot[c0], 32u);
+    } else if (ok) {
+      atomicAdd(&s_tot[c], 1u);
+    }
+    if (ok && ((r + half + 1u) & bmask) == 0u) atomicAdd(&s_last[c], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cells; i += blockDim.x) {
+    if (s_tot[i]) atomicAdd(&total[i], s_tot[i]);
+    if (s_last[i]) atomicAdd(&last[i], s_last[i]);
+  }
+}
+
 __global__ void greedy_rows(const uint32_t* __restrict__ prefix, uint32_t m, unsigned p, uint32_t* out) {
   const unsigned k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (k >= p) return;
@@ -688,26 +724,62 @@ int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned lb, unsigned p, Ar
 
   // row prefix + partition_rows_by_nnz (inc/bcoh.hpp:213-216); the greedy lower bounds run on the
   // device, the clamp chain (a few integer ops per band) on the host.
-  uint32_t* prefix = ar.alloc_n<uint32_t>((uint64_t)f.m + 1);
-  if (!prefix) return kNoMemory;
-  cudaMemsetAsync(prefix, 0, 4 * ((uint64_t)f.m + 1), s);
-  if (a.nnz) row_hist<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.row_ind, a.nnz, f.m, prefix);
-  exclusive_scan_u32(prefix, prefix, f.m, ar);
-  std::vector<uint32_t> greedy(p > 1 ? p - 1 : 1), bounds(p + 1);
-  uint32_t* d_greedy = ar.alloc_n<uint32_t>(p);
-  if (p > 1) greedy_rows<<<(p + 255) / 256, 256, 0, s>>>(prefix, f.m, p, d_greedy);
-  uint32_t total_nnz = 0;
-  cudaMemcpyAsync(&total_nnz, prefix + f.m, 4, cudaMemcpyDeviceToHost, s);
-  if (p > 1) cudaMemcpyAsync(greedy.data(), d_greedy, 4 * (p - 1), cudaMemcpyDeviceToHost, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("bcoh prefix");
+  // raw_cut[k-1] = (greedy row + beta/2) >> lb of partition_rows_by_nnz, from per-rounding-cell
+  // counts when they fit in shared memory, else from the full row prefix
+  std::vector<uint32_t> raw_cut(p > 1 ? p - 1 : 1), bounds(p + 1);
+  const uint32_t half = beta / 2;
+  const uint64_t cells = (((uint64_t)f.m + half) >> lb) + 1;
+  if (p > 1 && cells <= kMaxRoundCells) {
+    uint32_t* d_cell = ar.alloc_n<uint32_t>(2 * cells);
+    if (!d_cell) return kNoMemory;
+    cudaMemsetAsync(d_cell, 0, 8 * cells, s);
+    if (a.nnz)
+      round_cell_hist<<<grid_for(a.nnz, 256, kNumSMs * 4), 256, 0, s>>>(a.row_ind, a.nnz, f.m, lb, (uint32_t)cells,
+                                                                        d_cell, d_cell + cells);
+    std::vector<uint32_t> tot(cells), last(cells);
+    cudaMemcpyAsync(tot.data(), d_cell, 4 * cells, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(last.data(), d_cell + cells, 4 * cells, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("bcoh row cells");
+    uint64_t nnz_rows = 0;
+    for (uint32_t v : tot) nnz_rows += v;
+    // prefix[min(E_c - 1, m)] with E_c = (c+1) beta - beta/2, the rows before the cell's last row
+    std::vector<uint64_t> pre(cells);
+    uint64_t run = 0;
+    for (uint64_t c = 0; c < cells; ++c) {
+      const uint64_t end_row = (c + 1) * beta - half - 1;
+      pre[c] = end_row >= f.m ? nnz_rows : run + tot[c] - last[c];
+      run += tot[c];
+    }
+    for (unsigned k = 1; k < p; ++k) {  // smallest cell whose prefix reaches k * nnz / p
+      const uint64_t target = nnz_rows * k;
+      uint64_t lo = 0, hi = cells - 1;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (pre[mid] * p >= target) hi = mid; else lo = mid + 1;
+      }
+      raw_cut[k - 1] = (uint32_t)lo;
+    }
+  } else if (p > 1) {
+    uint32_t* prefix = ar.alloc_n<uint32_t>((uint64_t)f.m + 1);
+    uint32_t* d_greedy = ar.alloc_n<uint32_t>(p);
+    if (!prefix || !d_greedy) return kNoMemory;
+    cudaMemsetAsync(prefix, 0, 4 * ((uint64_t)f.m + 1), s);
+    if (a.nnz) row_hist<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.row_ind, a.nnz, f.m, prefix);
+    exclusive_scan_u32(prefix, prefix, f.m, ar);
+    greedy_rows<<<(p + 255) / 256, 256, 0, s>>>(prefix, f.m, p, d_greedy);
+    std::vector<uint32_t> greedy(p - 1);
+    cudaMemcpyAsync(greedy.data(), d_greedy, 4 * (p - 1), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("bcoh prefix");
+    for (unsigned k = 1; k < p; ++k) raw_cut[k - 1] = (uint32_t)(((uint64_t)greedy[k - 1] + half) >> lb);
+  }
   {
-    // Replays partition_rows_by_nnz with the device-computed greedy rows.
+    // Replays partition_rows_by_nnz's clamp chain (inc/block_size.hpp:86-98) on the raw cuts.
     const uint32_t block_rows = f.block_rows;
     for (unsigned k = 0; k <= p; ++k) bounds[k] = f.m;
     bounds[0] = 0;
     uint32_t prev_cut = 0;
     for (unsigned k = 1; k < p; ++k) {
-      uint32_t cut = (uint32_t)(((uint64_t)greedy[k - 1] + beta / 2) >> lb);
+      uint32_t cut = raw_cut[k - 1];
       const uint32_t hic = block_rows >= p ? block_rows - (p - k) : block_rows;
       const uint32_t loc = prev_cut + 1 < hic ? prev_cut + 1 : hic;
       if (cut < loc) cut = loc;

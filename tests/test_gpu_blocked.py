@@ -146,6 +146,21 @@ def test_window_and_reduction_kernels(cuda, oracle, monkeypatch, window):
         np.testing.assert_array_equal(sp.run_spmv(alg, fi, ones, p=1).cpu().numpy(), exact)
 
 
+@pytest.mark.parametrize("l2", [64, 4096])
+def test_bcoh_band_partition_paths(cuda, oracle, l2):
+    """The band cuts come from per-rounding-cell counts (few cells) or from the full row prefix
+    (beta = 2 on 16k rows: 8k cells); both must reproduce partition_rows_by_nnz exactly."""
+    sp = cuda
+    from paper_2502_19284_b200 import gen
+    m, n, r, c, v = gen.rmat_host(14, 4, seed=12)
+    a = _dev(sp, m, n, r, c, v)
+    for alg in BCOH:
+        for p in (2, 5):
+            ref = oracle.build(alg, m, n, r, c, v, threads=p, l2_bytes=l2)
+            f = sp.build_format(alg, a, p, sp.EngineOptions(l2_bytes=l2))
+            _check_format(sp, f, ref, alg, f"rmat14 alg {alg} p {p} l2 {l2}")
+
+
 def test_bcoh_band_mismatch(cuda):
     """spmv_parallel.hpp:339-341: BCOH multiply with p != bands is InvalidArgument."""
     sp = cuda
