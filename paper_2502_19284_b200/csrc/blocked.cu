@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
     const uint32_t* __restrict__ packed, const double* __restrict__ data,
     const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
     const uint2* __restrict__ blk_rc, const uint32_t* __restrict__ item_chunk,
-    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ item_whole, unsigned lb, uint32_t m,
-    const double* __restrict__ x, double* __restrict__ y) {
+    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ item_whole,
+    const uint32_t* __restrict__ ord, unsigned lb, uint32_t m, const double* __restrict__ x,
+    double* __restrict__ y) {
   extern __shared__ double win[];
   const uint32_t item = blockIdx.x;
   const uint32_t c0 = item_chunk[item], c1 = item_chunk[item + 1];
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
   __syncthreads();
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   constexpr int U = 8;  // 8 x 32 = one full chunk in flight per warp
-  for (uint32_t c = c0 + warp; c < c1; c += nwarps) {
+  for (uint32_t q = c0 + warp; q < c1; q += nwarps) {
+    const uint32_t c = ord ? ord[q] : q;  // chunks listed in block-row order (BCOH) or storage order
     const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
     const uint32_t cbase = blk_rc[ch_blk[c]].y << lb;
     for (uint32_t base = e0; base < e1; base += 32 * U) {
@@ -195,7 +197,8 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
     window_spmv_kernel<<<nitems, kWinThreads, smem, s>>>(
         f.find("packed")->as<uint32_t>(), f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
         f.find("chunk_blk")->as<uint32_t>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
-        f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(), f.log2_beta, f.m, x, y);
+        f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(),
+        f.find("win_chunk_order") ? f.find("win_chunk_order")->as<uint32_t>() : nullptr, f.log2_beta, f.m, x, y);
     timing_end(s);
     return check_launch("spmv_blocked(window)");
   }

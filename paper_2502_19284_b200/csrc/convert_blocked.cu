@@ -437,14 +437,21 @@ __global__ void chunk_fill(const uint32_t* __restrict__ blk_begin, uint32_t nblk
   }
 }
 
-// Window-item plan for the block-row window kernel (CSB / MergeB): items start at every block-row
-// change and every kWinChunks-th chunk, so an item never crosses a block row.
-__global__ void win_heads(const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc, uint32_t nchunks,
-                          uint32_t per_item, uint32_t* __restrict__ head) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  const bool row_start = c == 0 || blk_rc[ch_blk[c]].x != blk_rc[ch_blk[c - 1]].x;
-  head[c] = row_start ? 3u : (c % per_item == 0 ? 1u : 0u);
+__device__ __forceinline__ uint32_t win_br(const uint32_t* ord, const uint32_t* ch_blk, const uint2* blk_rc,
+                                           uint32_t q) {
+  return blk_rc[ch_blk[ord ? ord[q] : q]].x;
+}
+
+// Window-item plan over the chunk sequence q -> chunk ord[q] (identity when ord is null): items
+// start at every block-row change and every kWinChunks-th position, so an item never crosses a
+// block row.
+__global__ void win_heads(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ ch_blk,
+                          const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t per_item,
+                          uint32_t* __restrict__ head) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nchunks) return;
+  const bool row_start = q == 0 || win_br(ord, ch_blk, blk_rc, q) != win_br(ord, ch_blk, blk_rc, q - 1);
+  head[q] = row_start ? 3u : (q % per_item == 0 ? 1u : 0u);
 }
 
 __global__ void win_flag(const uint32_t* __restrict__ head, uint32_t nchunks, uint32_t* __restrict__ flag) {
@@ -453,17 +460,25 @@ __global__ void win_flag(const uint32_t* __restrict__ head, uint32_t nchunks, ui
 }
 
 __global__ void win_fill(const uint32_t* __restrict__ head, const uint32_t* __restrict__ scan,
-                         const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc, uint32_t nchunks,
-                         uint32_t* __restrict__ item_chunk, uint32_t* __restrict__ item_br,
-                         uint32_t* __restrict__ item_whole) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks || !head[c]) return;
-  const uint32_t i = scan[c];
-  uint32_t e = c + 1;
+                         const uint32_t* __restrict__ ord, const uint32_t* __restrict__ ch_blk,
+                         const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t* __restrict__ item_chunk,
+                         uint32_t* __restrict__ item_br, uint32_t* __restrict__ item_whole) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nchunks || !head[q]) return;
+  const uint32_t i = scan[q];
+  uint32_t e = q + 1;
   while (e < nchunks && !head[e]) ++e;
-  item_chunk[i] = c;
-  item_br[i] = blk_rc[ch_blk[c]].x;
-  item_whole[i] = (head[c] & 2u) && (e == nchunks || (head[e] & 2u)) ? 1u : 0u;
+  item_chunk[i] = q;
+  item_br[i] = win_br(ord, ch_blk, blk_rc, q);
+  item_whole[i] = (head[q] & 2u) && (e == nchunks || (head[e] & 2u)) ? 1u : 0u;
+}
+
+__global__ void win_order_keys(const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc,
+                               uint32_t nchunks, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  keys[c] = blk_rc[ch_blk[c]].x;
+  vals[c] = c;
 }
 
 int d2h_u32(const uint32_t* dev, uint32_t* host, cudaStream_t s) {
@@ -581,7 +596,10 @@ static int blocked_common(BlockedBuild& bb, const spmvlab_cuda_coo& a, const uin
 // is faster there (335 vs 465 us).  SPMVLAB_BLOCKED_WINDOW=0 disables, =1 forces for all four.
 constexpr uint32_t kWinChunks = 256;
 
-static int window_plan(Format& f, Arena& ar, bool curve_in_block) {
+// `permute`: the block rows are not contiguous in storage (BCOH's Hilbert-ordered blocks), so the
+// chunks are first listed in block-row order ("win_chunk_order", a stable sort of chunk ids by
+// block row) and the items are runs of that list.
+static int window_plan(Format& f, Arena& ar, bool curve_in_block, bool permute = false) {
   const char* env = std::getenv("SPMVLAB_BLOCKED_WINDOW");
   const bool want = env && env[0] ? env[0] == '1' : curve_in_block;
   if (!want || f.log2_beta > 14 || f.work_items == 0) return kOk;
@@ -592,7 +610,20 @@ static int window_plan(Format& f, Arena& ar, bool curve_in_block) {
   uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   if (!head || !flag) return kNoMemory;
-  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ch_blk, blk_rc, nch, kWinChunks, head);
+  const uint32_t* ord = nullptr;
+  if (permute) {
+    uint64_t* k1 = ar.alloc_n<uint64_t>(nch);
+    uint64_t* k2 = ar.alloc_n<uint64_t>(nch);
+    uint32_t* v2 = ar.alloc_n<uint32_t>(nch);
+    uint32_t* v1 = static_cast<uint32_t*>(f.add("win_chunk_order", nch, 4, s));
+    if (!k1 || !k2 || !v1 || !v2) return kNoMemory;
+    win_order_keys<<<(nch + 255) / 256, 256, 0, s>>>(ch_blk, blk_rc, nch, k1, v1);
+    const int brbits = std::max(1, (int)bit_width64(f.block_rows ? f.block_rows - 1 : 0));
+    if (radix_sort_pairs(k1, k2, v1, v2, nch, 0, brbits, ar))
+      cudaMemcpyAsync(v1, v2, 4ull * nch, cudaMemcpyDeviceToDevice, s);
+    ord = v1;
+  }
+  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, kWinChunks, head);
   win_flag<<<(nch + 255) / 256, 256, 0, s>>>(head, nch, flag);  // flag = head != 0
   exclusive_scan_u32(flag, flag, nch, ar);                        // -> item index of each head
   uint32_t nitems = 0;
@@ -602,7 +633,8 @@ static int window_plan(Format& f, Arena& ar, bool curve_in_block) {
   uint32_t* item_whole = static_cast<uint32_t*>(f.add("win_item_whole", nitems, 4, s));
   if (!item_chunk || !item_br || !item_whole) return kNoMemory;
   cudaMemcpyAsync(item_chunk + nitems, &nch, 4, cudaMemcpyHostToDevice, s);
-  win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ch_blk, blk_rc, nch, item_chunk, item_br, item_whole);
+  win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ord, ch_blk, blk_rc, nch, item_chunk, item_br,
+                                              item_whole);
   return check_launch("window_plan");
 }
 
@@ -943,6 +975,9 @@ int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned lb, unsigned p, Ar
   }
   f.arrays = sorted;
   f.nstorage = 8;
+  // Hilbert in-block (packed) variants: block-row windows over a block-row ordering of the chunks
+  if (a.nnz && helem)
+    if (int rc = window_plan(f, ar, true, true)) return rc;
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_bcoh");
   return check_launch("build_bcoh");
 }

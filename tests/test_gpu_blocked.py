@@ -131,7 +131,7 @@ def test_window_and_reduction_kernels(cuda, oracle, monkeypatch, window):
     ai = _dev(sp, m, n, r, c, vi)
     exact = oracle.spmv_triplet(m, r, c, vi, np.ones(n))
     ones = torch.ones(n, dtype=torch.float64, device="cuda")
-    for alg in (3, 4, 9, 10):
+    for alg in (3, 4, 9, 10, 7, 8):
         ref = oracle.build(alg, m, n, r, c, v, threads=1, l2_bytes=512 * 1024)
         f = sp.build_format(alg, a, 1, sp.EngineOptions(l2_bytes=512 * 1024))
         _check_format(sp, f, ref, alg, f"window {window} alg {alg}")
