@@ -603,7 +603,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
 // Merge-path tiles of 32 * IPT items per warp (the same partition and carry fix-up as the other
 // variants), the tile's elements walked in lane-blocked passes of 128 with two passes' loads and
 // gathers in flight.  No product staging: shared memory holds only the 128-entry row map.
-template <int IPT, int WARPS>
+template <int IPT, int WARPS, int NP>
 __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
@@ -621,14 +621,20 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
   uint32_t rp = r0;
   uint32_t prevE = __ldg(row_ptr + r0);
   double carry = 0.0;
-  for (uint32_t base = j0 & ~3u;; base += 256u) {
-    double pa[4], pb[4];
-    vec_products(col, val, x, base + 4 * lane, j0, j1, pf, pl, pa);
-    vec_products(col, val, x, base + 128u + 4 * lane, j0, j1, pf, pl, pb);
-    vec_pass(row_ptr, y, smap, base, j0, j1, r1, rp, prevE, pa, carry, lane);
-    if (!(base + 128u < j1 || rp < r1)) break;
-    vec_pass(row_ptr, y, smap, base + 128u, j0, j1, r1, rp, prevE, pb, carry, lane);
-    if (!(base + 256u < j1 || rp < r1)) break;
+  bool more = true;
+  for (uint32_t base = j0 & ~3u; more; base += 128u * NP) {
+    double p[NP][4];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
+        more = false;
+        break;
+      }
+      vec_pass(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane);
+    }
+    if (!(base + 128u * NP < j1 || rp < r1)) more = false;
   }
   if (lane == 0) {
     carry_row[t] = r1;
@@ -799,11 +805,11 @@ void launch_merge_wstage(const Format& f, const double* x, double* y, const Scra
                                                                                                f.merge_tiles);
 }
 
-template <int THREADS, int IPT>
+template <int THREADS, int IPT, int NP>
 void launch_merge_vec(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   constexpr int WARPS = THREADS / 32;
-  merge_spmv_vec_kernel<IPT, WARPS><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
-                                                                                            f.merge_tiles);
+  merge_spmv_vec_kernel<IPT, WARPS, NP><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
+                                                                                                f.merge_tiles);
 }
 
 template <int THREADS, int IPT>
@@ -875,13 +881,15 @@ bool merge_shape_supported(int threads, int ipt, int variant) {
 }
 
 uint32_t merge_tile_items(int threads, int ipt, int variant) {
-  const bool per_warp = variant == kVariantShuffle || variant == kVariantWarpStage || variant == kVariantVector;
+  const bool per_warp = variant == kVariantShuffle || variant == kVariantWarpStage || variant == kVariantVector ||
+                        variant == kVariantVector3;
   return (uint32_t)((per_warp ? 32 : threads) * ipt);
 }
 
 static const char* merge_kernel_name(int variant) {
   switch (variant) {
-    case kVariantVector: return "merge_spmv_vec_kernel";
+    case kVariantVector:
+    case kVariantVector3: return "merge_spmv_vec_kernel";
     case kVariantShuffle: return "merge_spmv_shfl_kernel";
     case kVariantWarpStage: return "merge_spmv_wstage_kernel";
     case kVariantTma: return "merge_spmv_tma_kernel";
@@ -893,7 +901,8 @@ template <int T, int I, int V>
 static void launch_merge_shape(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   if constexpr (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);
   else if constexpr (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s);
-  else if constexpr (V == kVariantVector) launch_merge_vec<T, I>(f, x, y, sc, s);
+  else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s);
+  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 3>(f, x, y, sc, s);
   else if constexpr (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s);
   else launch_merge_tma<T, I, 2>(f, x, y, sc, s);
 }
