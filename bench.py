@@ -214,7 +214,9 @@ def all_formats(sp, a, m, n, nnz, x, stream, peak, merge_us, threads=8):
         # conversion time = min of 3 builds (the reference protocol takes the min of its
         # conversion repetitions, inc/bench.hpp:315-318); the first build also warms the pools
         conv_ms = float("inf")
+        f = None
         for _ in range(3):
+            f = None  # release the previous build outside the timed region
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
