@@ -182,6 +182,40 @@ void spmvlab_cuda_free_host_coo(spmvlab_cuda_host_coo* a);
  * Market text; device buffers as in spmvlab_cuda_cache_read. */
 int spmvlab_cuda_load_matrix(const char* path, spmvlab_cuda_coo* a, void* stream);
 
+/* --- standalone ICRS / BICRS (inc/bicrs.hpp) --------------------------------------------------- */
+
+/* IncrementalRowStorage (bicrs.hpp:33-45) in device memory.  kind 0 = ICRS (u32 increments and
+ * row jumps, index_t), kind 1 = BICRS (i64, signed_index_t).  col_inc has nnz + 1 entries. */
+typedef struct {
+  uint32_t m, n;
+  uint64_t nnz;
+  int kind;
+  void* col_inc;
+  void* row_jump;
+  uint64_t n_row_jump;
+  double* data;
+} spmvlab_cuda_bicrs;
+
+/* crs_to_icrs (bicrs.hpp:120-150) from a CRS-family format (algorithms 0-2); library-allocated
+ * arrays, release with spmvlab_cuda_free_bicrs.  Bit-identical to the reference. */
+int spmvlab_cuda_crs_to_icrs(const spmvlab_cuda_format* crs, spmvlab_cuda_bicrs* out, void* stream);
+
+/* triplet_to_bicrs (bicrs.hpp:154-200) with the elements in `order` (device, a permutation of
+ * [0, nnz); otherwise InvalidArgument). */
+int spmvlab_cuda_triplet_to_bicrs(const spmvlab_cuda_coo* a, const uint32_t* order, spmvlab_cuda_bicrs* out,
+                                  void* stream);
+
+/* spmv_bicrs_seq (bicrs.hpp:98-109): y (length m) fully overwritten; stats_host (2 entries, may be
+ * NULL) = ReplayStats {overflow_events, row_jumps_consumed}.  DimensionMismatch, CorruptFormat. */
+int spmvlab_cuda_bicrs_spmv(const spmvlab_cuda_bicrs* a, const double* x, uint64_t x_len, double* y,
+                            uint64_t y_len, uint64_t* stats_host, void* stream);
+
+/* bicrs_to_triplet (bicrs.hpp:111-118): row and column of every element (device, nnz each); the
+ * values are a->data.  CorruptFormat. */
+int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, uint32_t* cols, void* stream);
+
+void spmvlab_cuda_free_bicrs(spmvlab_cuda_bicrs* a);
+
 /* --- primitives, exposed for parity tests ---------------------------------------------------- */
 
 /* select_block_size -- inc/block_size.hpp:47-61 (value_size 8). Host computation. */

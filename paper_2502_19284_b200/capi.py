@@ -23,8 +23,16 @@ EXPORTS = [
     "spmvlab_cuda_launch_count", "spmvlab_cuda_kernel_timing", "spmvlab_cuda_kernel_time",
     "spmvlab_cuda_cache_read", "spmvlab_cuda_cache_write", "spmvlab_cuda_free_coo", "spmvlab_cuda_cache_info",
     "spmvlab_cuda_iterate", "spmvlab_cuda_read_matrix_market", "spmvlab_cuda_read_matrix_market_host",
-    "spmvlab_cuda_free_host_coo", "spmvlab_cuda_load_matrix",
+    "spmvlab_cuda_free_host_coo", "spmvlab_cuda_load_matrix", "spmvlab_cuda_crs_to_icrs",
+    "spmvlab_cuda_triplet_to_bicrs", "spmvlab_cuda_bicrs_spmv", "spmvlab_cuda_bicrs_to_triplet",
+    "spmvlab_cuda_free_bicrs",
 ]
+
+
+class Bicrs(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("n", C.c_uint32), ("nnz", C.c_uint64), ("kind", C.c_int),
+                ("col_inc", C.c_void_p), ("row_jump", C.c_void_p), ("n_row_jump", C.c_uint64),
+                ("data", C.c_void_p)]
 
 
 class MmHeader(C.Structure):
@@ -80,6 +88,12 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_free_host_coo.argtypes = [C.POINTER(HostCoo)]
     L.spmvlab_cuda_free_host_coo.restype = None
     L.spmvlab_cuda_load_matrix.argtypes = [C.c_char_p, C.POINTER(Coo), vp]
+    L.spmvlab_cuda_crs_to_icrs.argtypes = [vp, C.POINTER(Bicrs), vp]
+    L.spmvlab_cuda_triplet_to_bicrs.argtypes = [C.POINTER(Coo), vp, C.POINTER(Bicrs), vp]
+    L.spmvlab_cuda_bicrs_spmv.argtypes = [C.POINTER(Bicrs), vp, u64, vp, u64, vp, vp]
+    L.spmvlab_cuda_bicrs_to_triplet.argtypes = [C.POINTER(Bicrs), vp, vp, vp]
+    L.spmvlab_cuda_free_bicrs.argtypes = [C.POINTER(Bicrs)]
+    L.spmvlab_cuda_free_bicrs.restype = None
     L.spmvlab_cuda_run_spmv_host.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp, vp, vp]
     L.spmvlab_cuda_storage_report.argtypes = [vp, C.POINTER(StorageArray), C.c_size_t, C.POINTER(C.c_size_t)]
     L.spmvlab_cuda_get_format_info.argtypes = [vp, C.POINTER(FormatInfo)]

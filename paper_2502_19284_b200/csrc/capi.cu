@@ -483,6 +483,51 @@ int spmvlab_cuda_load_matrix(const char* path, spmvlab_cuda_coo* a, void* stream
   return load_matrix(path, a, static_cast<cudaStream_t>(stream));
 }
 
+int spmvlab_cuda_crs_to_icrs(const spmvlab_cuda_format* crs, spmvlab_cuda_bicrs* out, void* stream) {
+  if (!crs || !out) return fail(kInvalidArgument, "null argument");
+  if (!is_crs_alg(crs->alg)) return fail(kInvalidArgument, "format is not CRS");
+  g_last_error.clear();
+  std::memset(out, 0, sizeof(*out));
+  return crs_to_icrs(*crs, out, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_triplet_to_bicrs(const spmvlab_cuda_coo* a, const uint32_t* order, spmvlab_cuda_bicrs* out,
+                                  void* stream) {
+  if (!a || !out || (a->nnz && !order)) return fail(kInvalidArgument, "null argument");
+  if ((uint64_t)a->m > (1ull << 31) || (uint64_t)a->n > (1ull << 31))
+    return fail(kOverflow, "matrix dimension exceeds the supported index width");
+  g_last_error.clear();
+  std::memset(out, 0, sizeof(*out));
+  return triplet_to_bicrs(*a, order, out, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_bicrs_spmv(const spmvlab_cuda_bicrs* a, const double* x, uint64_t x_len, double* y,
+                            uint64_t y_len, uint64_t* stats_host, void* stream) {
+  if (!a) return fail(kInvalidArgument, "null argument");
+  if (x_len != a->n)
+    return fail(kDimensionMismatch, "x has length " + std::to_string(x_len) + ", matrix has " +
+                                        std::to_string(a->n) + " columns");
+  if (y_len != a->m)
+    return fail(kDimensionMismatch, "y has length " + std::to_string(y_len) + ", matrix has " +
+                                        std::to_string(a->m) + " rows");
+  g_last_error.clear();
+  return bicrs_spmv(*a, x, y, stats_host, static_cast<cudaStream_t>(stream));
+}
+
+int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, uint32_t* cols, void* stream) {
+  if (!a || (a->nnz && (!rows || !cols))) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return bicrs_decode_all(*a, rows, cols, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+void spmvlab_cuda_free_bicrs(spmvlab_cuda_bicrs* a) {
+  if (!a) return;
+  cudaFree(a->col_inc);
+  cudaFree(a->row_jump);
+  cudaFree(a->data);
+  std::memset(a, 0, sizeof(*a));
+}
+
 uint64_t spmvlab_cuda_launch_count(void) { return g_launches.load(); }
 
 void spmvlab_cuda_kernel_timing(int enable) {

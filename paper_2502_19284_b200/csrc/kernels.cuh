@@ -59,6 +59,10 @@ int cache_write(const char* path, const spmvlab_cuda_coo& a, cudaStream_t s);
 int mm_read_host(const char* path, spmvlab_cuda_host_coo* out, spmvlab_cuda_mm_header* header);
 int mm_read_device(const char* path, spmvlab_cuda_coo* a, spmvlab_cuda_mm_header* header, cudaStream_t s);
 int load_matrix(const char* path, spmvlab_cuda_coo* a, cudaStream_t s);
+int crs_to_icrs(const Format& f, spmvlab_cuda_bicrs* out, cudaStream_t s);
+int triplet_to_bicrs(const spmvlab_cuda_coo& a, const uint32_t* order, spmvlab_cuda_bicrs* out, cudaStream_t s);
+int bicrs_decode_all(const spmvlab_cuda_bicrs& b, uint32_t* rows, uint32_t* cols, uint64_t* stats, cudaStream_t s);
+int bicrs_spmv(const spmvlab_cuda_bicrs& b, const double* x, double* y, uint64_t* stats, cudaStream_t s);
 
 // ---- instrumentation: launch counter and dominant-kernel event brackets (capi.cu)
 void note_launch(unsigned n = 1);

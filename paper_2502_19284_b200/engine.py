@@ -393,6 +393,104 @@ def load_matrix(path: str, stream=None) -> TripletMatrix:
     return a
 
 
+def _view_copy(ptr, count: int, typestr: str, dtype, dev) -> torch.Tensor:
+    """Copy of `count` elements of library device memory into a torch tensor."""
+    out = torch.empty(count, dtype=dtype, device=dev)
+    if count:
+        class _V:
+            def __init__(self):
+                self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+        out.copy_(torch.as_tensor(_V(), device=dev))
+    return out
+
+
+class IncrementalRowStorage:
+    """IncrementalRowStorage (inc/bicrs.hpp:33-45) on the device: ICRS (kind 0, u32 increments)
+    or BICRS (kind 1, i64 increments).  Owns the library arrays."""
+
+    def __init__(self, c: "capi.Bicrs", keep=None):
+        self._c = c
+        self._keep = keep  # torch tensors backing the arrays (then the library does not own them)
+
+    kind = property(lambda self: int(self._c.kind))
+    m = property(lambda self: int(self._c.m))
+    n = property(lambda self: int(self._c.n))
+
+    def nnz(self) -> int:
+        return int(self._c.nnz)
+
+    def arrays(self) -> dict:
+        """Host copies: col_inc (nnz + 1), row_jump, data (numpy)."""
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ts, dt = ("<u4", torch.int32) if self.kind == 0 else ("<i8", torch.int64)
+        ci = _view_copy(self._c.col_inc, self.nnz() + 1, ts, dt, dev).cpu().numpy()
+        rj = _view_copy(self._c.row_jump, int(self._c.n_row_jump), ts, dt, dev).cpu().numpy()
+        if self.kind == 0:
+            ci, rj = ci.view(np.uint32), rj.view(np.uint32)
+        data = _view_copy(self._c.data, self.nnz(), "<f8", torch.float64, dev).cpu().numpy()
+        return {"col_inc": ci, "row_jump": rj, "data": data}
+
+    def spmv(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
+        """spmv_bicrs_seq (inc/bicrs.hpp:98-109) -> (y, (overflow_events, row_jumps_consumed))."""
+        if y is None:
+            y = torch.empty(self.m, dtype=torch.float64, device=x.device)
+        stats = (C.c_uint64 * 2)()
+        _check(capi.load().spmvlab_cuda_bicrs_spmv(C.byref(self._c), x.data_ptr(), x.numel(), y.data_ptr(),
+                                                   y.numel(), stats, _stream(stream)))
+        return y, (int(stats[0]), int(stats[1]))
+
+    def to_triplet(self, stream=None):
+        """bicrs_to_triplet (inc/bicrs.hpp:111-118) -> device (rows, cols) in element order."""
+        dev = torch.device("cuda", torch.cuda.current_device())
+        k = self.nnz()
+        rows = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        cols = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        _check(capi.load().spmvlab_cuda_bicrs_to_triplet(C.byref(self._c), rows.data_ptr(), cols.data_ptr(),
+                                                         _stream(stream)))
+        return rows[:k], cols[:k]
+
+    def close(self):
+        if self._c is not None and self._keep is None:
+            capi.load().spmvlab_cuda_free_bicrs(C.byref(self._c))
+        self._c = None
+        self._keep = None
+
+    __del__ = close
+
+
+def crs_to_icrs(fmt: BuiltFormat, stream=None) -> IncrementalRowStorage:
+    """crs_to_icrs (inc/bicrs.hpp:120-150) from a CRS-family format."""
+    c = capi.Bicrs()
+    _check(capi.load().spmvlab_cuda_crs_to_icrs(fmt.handle, C.byref(c), _stream(stream)))
+    return IncrementalRowStorage(c)
+
+
+def triplet_to_bicrs(a: TripletMatrix, order: torch.Tensor, stream=None) -> IncrementalRowStorage:
+    """triplet_to_bicrs (inc/bicrs.hpp:154-200) with the elements in `order` (device int32)."""
+    c = capi.Bicrs()
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_triplet_to_bicrs(C.byref(coo), order.data_ptr() if order.numel() else None,
+                                                     C.byref(c), _stream(stream)))
+    return IncrementalRowStorage(c)
+
+
+def bicrs_from_arrays(m: int, n: int, col_inc, row_jump, data, kind: int = 1) -> IncrementalRowStorage:
+    """Wraps host arrays (e.g. a stream from elsewhere) as a device ICRS / BICRS for the multiply
+    and the replay checks (device copies held by torch)."""
+    dt = np.uint32 if kind == 0 else np.int64
+    ci = np.ascontiguousarray(col_inc, dtype=dt)
+    rj = np.ascontiguousarray(row_jump, dtype=dt)
+    dv = np.ascontiguousarray(data, dtype=np.float64)
+    if len(ci) != len(dv) + 1:  # replay_bicrs, inc/bicrs.hpp:58-59
+        raise Error(ErrorKind.CorruptFormat, "col_inc must hold nnz + 1 entries")
+    to = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda()
+    tci, trj, tdv = to(ci), to(rj), to(dv)
+    ptr = lambda t: t.data_ptr() if t.numel() else None
+    c = capi.Bicrs(m, n, len(dv), kind, ptr(tci), ptr(trj), len(rj), ptr(tdv))
+    return IncrementalRowStorage(c, keep=(tci, trj, tdv))
+
+
 def cache_write(path: str, a: TripletMatrix, stream=None) -> None:
     """Device triplet -> SPMVLAB1 cache, byte-identical to the reference's cache_write."""
     coo = a._c()
