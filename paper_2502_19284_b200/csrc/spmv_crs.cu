@@ -566,7 +566,8 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   }
   __syncwarp();
   int4 m4 = *reinterpret_cast<int4*>(smap + 4 * lane);
-  *reinterpret_cast<int4*>(smap + 4 * lane) = make_int4(-1, -1, -1, -1);
+  if ((m4.x & m4.y & m4.z & m4.w) != -1)  // only lanes whose entries were set clear them
+    *reinterpret_cast<int4*>(smap + 4 * lane) = make_int4(-1, -1, -1, -1);
   const int rid[4] = {m4.x, m4.y, m4.z, m4.w};
   double run = 0.0, first_val = 0.0;
   int first_row = -1;
@@ -586,6 +587,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   const unsigned heads = __ballot_sync(0xFFFFFFFFu, first_row >= 0);
   const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
   const int seg = heads & le ? 31 - __clz(heads & le) : 0;
+  // (a data-dependent depth -- log2 of the longest segment -- measured slower: 313 vs 292 us)
   double v = run;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
