@@ -19,7 +19,7 @@ constexpr int kVariantTma = 1;
 constexpr int kVariantShuffle = 2;
 constexpr int kVariantWarpStage = 3;
 constexpr int kVariantVector = 4;   // lane-blocked passes, two passes in flight
-constexpr int kVariantVector3 = 5;  // three passes in flight: spills at 40 registers, 345 us (not instantiated)
+constexpr int kVariantVector3 = 5;  // the same, next pass's col_ind quad prefetched
 constexpr int kMergeThreads = 256;
 constexpr int kMergeIpt = 32;  // upper bound; build_merge_plan picks 32 / 16 / 8 by matrix size
 constexpr int kMergeVariant = kVariantVector;

@@ -539,6 +539,32 @@ __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, c
   }
 }
 
+// Split form for software pipelining: the col_ind quad of a later pass is loaded early
+// (vec_cols) so its x gathers issue as soon as that pass starts (vec_products_c).
+__device__ __forceinline__ uint4 vec_cols(const uint32_t* __restrict__ col, uint32_t k, uint32_t j0, uint32_t j1,
+                                          uint64_t pf) {
+  return (k >= j0 && k + 3 < j1) ? ld_stream4(col + k, pf) : make_uint4(0u, 0u, 0u, 0u);
+}
+__device__ __forceinline__ void vec_products_c(const uint32_t* __restrict__ col, const double* __restrict__ val,
+                                               const double* __restrict__ x, uint32_t k, uint32_t j0, uint32_t j1,
+                                               uint64_t pf, uint64_t pl, uint4 c, double p[4]) {
+  if (k >= j0 && k + 3 < j1) {
+    double v0, v1, v2, v3;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
+    p[0] = v0 * ld_x(x + c.x, pl);
+    p[1] = v1 * ld_x(x + c.y, pl);
+    p[2] = v2 * ld_x(x + c.z, pl);
+    p[3] = v3 * ld_x(x + c.w, pl);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t e = k + u;
+      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * ld_x(x + ld_stream(col + e, pf), pl) : 0.0;
+    }
+  }
+}
+
 // One 128-element pass of a warp tile.  Row ends falling in the pass are read 32 at a time from
 // row_ptr and scattered to the element they close (smap: element -> row, -1 = none); each lane
 // then walks its 4 products in registers, stores rows that close inside the lane, and the lane
@@ -606,7 +632,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
 // variants), the tile's elements walked in lane-blocked passes of 128 with two passes' loads and
 // gathers in flight.  No product staging: shared memory holds only the 128-entry row map.
 template <int IPT, int WARPS, int NP>
-__global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
+__global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
@@ -624,19 +650,29 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
   uint32_t prevE = __ldg(row_ptr + r0);
   double carry = 0.0;
   bool more = true;
-  for (uint32_t base = j0 & ~3u; more; base += 128u * NP) {
-    double p[NP][4];
+  uint4 cn[NP];  // NP == 1 selects the col_ind-prefetching form: next pass's quad loaded early
+  if (NP == 1) cn[0] = vec_cols(col, (j0 & ~3u) + 4 * lane, j0, j1, pf);
+  for (uint32_t base = j0 & ~3u; more; base += 128u * (NP == 1 ? 2 : NP)) {
+    constexpr int NPP = NP == 1 ? 2 : NP;
+    double p[NPP][4];
+    if constexpr (NP == 1) {
+      const uint4 cb = vec_cols(col, base + 128u + 4 * lane, j0, j1, pf);
+      vec_products_c(col, val, x, base + 4 * lane, j0, j1, pf, pl, cn[0], p[0]);
+      cn[0] = vec_cols(col, base + 256u + 4 * lane, j0, j1, pf);
+      vec_products_c(col, val, x, base + 128u + 4 * lane, j0, j1, pf, pl, cb, p[1]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < NP; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+      for (int i = 0; i < NP; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+    }
 #pragma unroll
-    for (int i = 0; i < NP; ++i) {
+    for (int i = 0; i < NPP; ++i) {
       if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
         more = false;
         break;
       }
       vec_pass(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane);
     }
-    if (!(base + 128u * NP < j1 || rp < r1)) more = false;
+    if (!(base + 128u * NPP < j1 || rp < r1)) more = false;
   }
   if (lane == 0) {
     carry_row[t] = r1;
@@ -904,7 +940,7 @@ static void launch_merge_shape(const Format& f, const double* x, double* y, cons
   if constexpr (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);
   else if constexpr (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s);
   else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s);
-  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 3>(f, x, y, sc, s);
+  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 1>(f, x, y, sc, s);  // col prefetch
   else if constexpr (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s);
   else launch_merge_tma<T, I, 2>(f, x, y, sc, s);
 }
