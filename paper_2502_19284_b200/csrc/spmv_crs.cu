@@ -518,6 +518,18 @@ __global__ void __launch_bounds__(WARPS * 32, (IPT <= 7 ? 48 : 32) / WARPS) merg
 // 4 consecutive nonzeros of a 128-element pass per lane, loaded with one 128-bit col_ind load and
 // one 256-bit data load (sm_100 ld.global.v4.f64); the products never leave registers.  Elements
 // outside [j0, j1) are masked (the tile's merge-path element range is not 4-aligned).
+// x gathers of the vector kernel; -DSPMV_XG_CG makes them L2-only (.cg): 384 vs 292 us at cfg2,
+// the 13 % L1 hit rate of R-MAT's hot columns is worth keeping.
+__device__ __forceinline__ double ld_xg(const double* p, uint64_t pol) {
+#ifdef SPMV_XG_CG
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return ld_x(p, pol);
+#endif
+}
+
 __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, const double* __restrict__ val,
                                              const double* __restrict__ x, uint32_t k, uint32_t j0, uint32_t j1,
                                              uint64_t pf, uint64_t pl, double p[4]) {
@@ -526,10 +538,10 @@ __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, c
     double v0, v1, v2, v3;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                  : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
-    p[0] = v0 * ld_x(x + c.x, pl);
-    p[1] = v1 * ld_x(x + c.y, pl);
-    p[2] = v2 * ld_x(x + c.z, pl);
-    p[3] = v3 * ld_x(x + c.w, pl);
+    p[0] = v0 * ld_xg(x + c.x, pl);
+    p[1] = v1 * ld_xg(x + c.y, pl);
+    p[2] = v2 * ld_xg(x + c.z, pl);
+    p[3] = v3 * ld_xg(x + c.w, pl);
   } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
