@@ -187,11 +187,8 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (const DevArray* items = f.find("win_item_chunk")) {
     const uint32_t nitems = (uint32_t)(items->count() - 1);
     const size_t smem = sizeof(double) << f.log2_beta;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(window_spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
+    once_per_device(
+        [] { cudaFuncSetAttribute(window_spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
     note_launch();
     timing_begin("window_spmv_kernel", s);
     window_spmv_kernel<<<nitems, kWinThreads, smem, s>>>(

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/spmvlab_cuda.h"

@@ -25,9 +25,9 @@ int check_launch(const char* what) {
 }
 
 void pool_init() {
-  static const bool ready = [] {
-    // Keep freed scratch in the device's default stream-ordered pool between builds instead of
-    // returning it to the driver at every synchronisation (conversions allocate GBs of keys).
+  // Keep freed scratch in each device's default stream-ordered pool between builds instead of
+  // returning it to the driver at every synchronisation (conversions allocate GBs of keys).
+  once_per_device([] {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
@@ -35,9 +35,7 @@ void pool_init() {
       uint64_t threshold = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
     }
-    return true;
-  }();
-  (void)ready;
+  });
 }
 
 void* Arena::alloc(size_t bytes) {
@@ -457,11 +455,8 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, V* vals, V* vals_alt,
   uint64_t* status = arena.alloc_n<uint64_t>(tiles * 256 + 8);
   uint32_t* counter = reinterpret_cast<uint32_t*>(status + tiles * 256);
   constexpr size_t smem = OneSweep<V>::SMEM;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(rs_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  once_per_device(
+      [] { cudaFuncSetAttribute(rs_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   bool in_alt = false;
   for (int p = 0; p < npasses; ++p) {
     const int shift = begin_bit + 8 * p;

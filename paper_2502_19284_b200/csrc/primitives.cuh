@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <mutex>
 #include <vector>
 
 namespace spmvcu {
@@ -42,5 +43,22 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, Arena& ar
 
 // Launch-error check helper: returns 0 or kCudaError and records the message.
 int check_launch(const char* what);
+
+// Runs `setup` once per (call site, current device), thread-safe: kernel attributes such as the
+// dynamic shared-memory limit are per device, and a concurrent first launch must not race ahead
+// of them.
+template <typename F>
+inline void once_per_device(F&& setup) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!(done & bit)) {
+    setup();
+    done |= bit;
+  }
+}
 
 }  // namespace spmvcu

@@ -875,12 +875,13 @@ template <int THREADS, int IPT, int STAGES>
 void launch_merge_tma(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
   using Cfg = MergeTmaCfg<THREADS, IPT, STAGES>;
   auto kern = merge_spmv_tma_kernel<THREADS, IPT, STAGES>;
-  static int grid_per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, Cfg::SMEM);
-    return occ > 0 ? occ : 1;
-  }();
+  once_per_device([] {
+    cudaFuncSetAttribute(merge_spmv_tma_kernel<THREADS, IPT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM);
+  });
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, Cfg::SMEM);
+  const int grid_per_sm = occ > 0 ? occ : 1;
   int dev = 0, sms = kNumSMs;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
