@@ -252,6 +252,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-formats", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: exchange fused into the multiply (default) or NCCL all-gatherv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -304,9 +306,23 @@ def main():
     y_loc = y_full[cuts[rank]:cuts[rank + 1]] if world > 1 else y_full
 
     sharded = sdist.ShardedSpMV(cuts, rank, lambda xf, yl: sp.run_spmv(sp.Algorithm.Merge, fmt, xf, yl, p=1))
+    fused, exchange = None, "none (1 GPU)"
+    if world > 1:
+        exchange = "NCCL all-gatherv (per-rank broadcasts) of the y slices"
+        if args.exchange == "fused":
+            try:  # collective; every rank agrees on success or falls back together
+                fused = sdist.FusedExchangeSpMV(cuts, rank, fmt, n)
+                fused.load(x)
+                exchange = "fused: merge-kernel epilogue stores rows into every rank's next x (CUDA IPC, NVLink)"
+            except Exception as ex:
+                log(f"fused exchange unavailable, using NCCL: {ex}")
+                fused = None
+                exchange += f" (fused unavailable: {ex})"
 
     def step():
-        if world > 1:
+        if fused is not None:
+            fused.step()  # x_next = A_r x on every rank: multiply + peer stores + rank barrier
+        elif world > 1:
             sharded.step(x, y_full)  # local merge-CSR multiply + NCCL all-gatherv of the y slices
         else:
             sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
@@ -452,11 +468,13 @@ def main():
                 "data": "synthetic (seeded, generated on device)",
                 "config": {"workload": CONFIG_DESC[args.config], "matrix": name, "n": n, "nnz": nnz_total,
                            "engine": "merge-CSR (spmv_merge)",
-                           "parallelism": f"row-shard x{world} + NCCL all-gather of y" if world > 1 else "1 GPU",
+                           "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU", "exchange": exchange,
                            "l2": "inputs larger than L2 (no flush)", "conversion_ms": conv_ms},
                 "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "formats": formats, "iterate": iterate}
         print(json.dumps(line), flush=True)
+    if fused is not None:
+        fused.close()  # collective
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -101,6 +101,25 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
 int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, double* work, uint32_t iters,
                          unsigned p, int flags, double* norms, void* stream);
 
+/* --- fused multi-GPU exchange (SURVEY.md §8e stretch: the y slices written straight into the
+ * peers' x over NVLink instead of a separate all-gather) ------------------------------------- */
+
+/* Exchange buffers: plain device allocations that can be mapped into the other ranks' processes
+ * through CUDA IPC.  alloc fills a 64-byte IPC handle; open maps a peer's handle (peer access
+ * enabled lazily); close unmaps (opened != 0) or frees. */
+int spmvlab_cuda_exchange_alloc(uint64_t bytes, void** dev_ptr, unsigned char ipc_handle[64]);
+int spmvlab_cuda_exchange_open(const unsigned char ipc_handle[64], void** dev_ptr);
+int spmvlab_cuda_exchange_close(void* dev_ptr, int opened);
+
+/* Merge-CSR multiply (algorithm 2) of a row shard whose epilogue also stores every finished row
+ * r of y into dest[i][row_offset + r] for i < ndest (<= 8; device pointers valid in this process,
+ * e.g. the peers' next-x buffers opened above): the all-gather of the y slices fused into the
+ * multiply.  y (length m) is written as by run_spmv.  Synchronise the ranks before reading the
+ * destinations. */
+int spmvlab_cuda_run_spmv_scatter(const spmvlab_cuda_format* f, const double* x, uint64_t x_len, double* y,
+                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t row_offset,
+                                  void* stream);
+
 /* storage_report(const BuiltFormat&) -- inc/engine.hpp:158-160 / inc/storage.hpp:62-123. */
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,
                                 size_t capacity, size_t* count);

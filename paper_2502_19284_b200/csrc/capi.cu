@@ -337,6 +337,56 @@ int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, doubl
   return rc;
 }
 
+int spmvlab_cuda_exchange_alloc(uint64_t bytes, void** dev_ptr, unsigned char ipc_handle[64]) {
+  if (!dev_ptr || !ipc_handle) return fail(kInvalidArgument, "null argument");
+  *dev_ptr = nullptr;
+  if (cudaMalloc(dev_ptr, bytes ? bytes : 8) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(kNoMemory, "device allocation failed (exchange buffer)");
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *dev_ptr) != cudaSuccess) {
+    cudaFree(*dev_ptr);
+    *dev_ptr = nullptr;
+    return check_launch("cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+  std::memcpy(ipc_handle, &h, 64);
+  return kOk;
+}
+
+int spmvlab_cuda_exchange_open(const unsigned char ipc_handle[64], void** dev_ptr) {
+  if (!dev_ptr || !ipc_handle) return fail(kInvalidArgument, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, 64);
+  if (cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    *dev_ptr = nullptr;
+    return check_launch("cudaIpcOpenMemHandle");
+  }
+  return kOk;
+}
+
+int spmvlab_cuda_exchange_close(void* dev_ptr, int opened) {
+  if (!dev_ptr) return kOk;
+  if (opened ? cudaIpcCloseMemHandle(dev_ptr) != cudaSuccess : cudaFree(dev_ptr) != cudaSuccess)
+    return check_launch("exchange_close");
+  return kOk;
+}
+
+int spmvlab_cuda_run_spmv_scatter(const spmvlab_cuda_format* f, const double* x, uint64_t x_len, double* y,
+                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t row_offset,
+                                  void* stream) {
+  if (!f) return fail(kInvalidArgument, "null format");
+  if (!is_crs_alg(f->alg)) return fail(kInvalidArgument, "format is not CRS");
+  if (x_len != f->n || y_len != f->m) return fail(kDimensionMismatch, "x / y length does not match the matrix");
+  if (ndest > kMaxRowDest || (ndest && !dest)) return fail(kInvalidArgument, "bad destination list");
+  RowDest d{};
+  for (unsigned i = 0; i < ndest; ++i) d.p[i] = dest[i];
+  d.n = ndest;
+  d.off = row_offset;
+  return spmv_merge(*f, x, y, static_cast<cudaStream_t>(stream), &d);
+}
+
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,
                                 size_t capacity, size_t* count) {
   if (!f) return fail(kInvalidArgument, "null format");

@@ -37,10 +37,27 @@ int build_csb(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, bool hil
 int build_mergeb(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, bool hilbert, Arena& ar);
 int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned log2_beta, unsigned p, Arena& ar);
 
+// Extra destinations of every finished y row (the fused multi-GPU exchange): row r is also stored
+// to p[i][off + r] for i < n -- peers' x buffers mapped through CUDA IPC, written over NVLink.
+constexpr unsigned kMaxRowDest = 8;
+struct RowDest {
+  double* p[kMaxRowDest];
+  unsigned n;
+  uint64_t off;
+};
+// SCATTER = false compiles to the plain store (the destination list is then never touched, so the
+// kernels keep their register / stack budget); kernels take the list as __grid_constant__.
+template <bool SCATTER>
+__device__ __forceinline__ void put_row(double* y, const RowDest& d, uint32_t r, double v) {
+  y[r] = v;
+  if constexpr (SCATTER)
+    for (unsigned i = 0; i < d.n; ++i) d.p[i][d.off + r] = v;
+}
+
 // ---- multiplies (stream-ordered; y fully overwritten)
 int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s);
 int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s);
-int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s);
+int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest = nullptr);
 int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s);
 
 // ---- iterated multiply (iterate.cu): x <- A x, `iters` times, with optional norms / rescaling

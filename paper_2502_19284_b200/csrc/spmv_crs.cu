@@ -585,9 +585,11 @@ __device__ __forceinline__ void vec_products_c(const uint32_t* __restrict__ col,
 // row_ptr and scattered to the element they close (smap: element -> row, -1 = none); each lane
 // then walks its 4 products in registers, stores rows that close inside the lane, and the lane
 // tails are combined by one warp segmented scan (carry = the open row's running sum).
+template <bool SCATTER>
 __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, double* __restrict__ y, int* smap,
                                          uint32_t base, uint32_t j0, uint32_t j1, uint32_t r1, uint32_t& rp,
-                                         uint32_t& prevE, const double p[4], double& carry, unsigned lane) {
+                                         uint32_t& prevE, const double p[4], double& carry, unsigned lane,
+                                         const RowDest& dest) {
   const uint32_t pend = min(base + 128u, j1);
   while (rp < r1) {
     const uint32_t idx = rp + lane;
@@ -597,7 +599,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
     if (lane == 0) S = prevE;
     const bool in = have && E <= pend;
     if (in) {
-      if (E == S || E <= j0) y[idx] = 0.0;  // empty row, or a row whose elements precede the tile
+      if (E == S || E <= j0) put_row<SCATTER>(y, dest, idx, 0.0);  // empty, or elements precede the tile
       else smap[E - 1 - base] = (int)idx;   // closes at element E - 1 of this pass
     }
     const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
@@ -621,7 +623,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
         first_row = rid[u];
         first_val = run;
       } else {
-        y[rid[u]] = run;
+        put_row<SCATTER>(y, dest, rid[u], run);
       }
       run = 0.0;
     }
@@ -638,7 +640,8 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   }
   double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
   if (lane == 0) ex = 0.0;
-  if (first_row >= 0) y[first_row] = first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry);
+  if (first_row >= 0)
+    put_row<SCATTER>(y, dest, first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
   const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
   carry = heads ? v31 : carry + v31;
   __syncwarp();
@@ -647,12 +650,12 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
 // Merge-path tiles of 32 * IPT items per warp (the same partition and carry fix-up as the other
 // variants), the tile's elements walked in lane-blocked passes of 128 with two passes' loads and
 // gathers in flight.  No product staging: shared memory holds only the 128-entry row map.
-template <int IPT, int WARPS, int NP>
+template <int IPT, int WARPS, int NP, bool SCATTER>
 __global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
-    double* __restrict__ carry_val, uint32_t tiles) {
+    double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest) {
   __shared__ __align__(16) int s_map_all[WARPS][128];
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t t = blockIdx.x * WARPS + warp;
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge
         more = false;
         break;
       }
-      vec_pass(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane);
+      vec_pass<SCATTER>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane, dest);
     }
     if (!(base + 128u * NPP < j1 || rp < r1)) more = false;
   }
@@ -795,9 +798,10 @@ __global__ void __launch_bounds__(THREADS, 2) merge_spmv_tma_kernel(
 // starts in the chunk and continues past it is finished by the whole warp sweeping the following
 // carries 32 at a time.  Runs that started in an earlier chunk are left to that chunk's warp.
 // Deterministic (fixed reduction order) and O(run / 32) dependent steps for the longest rows.
+template <bool SCATTER>
 __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
                                    const double* __restrict__ carry_val, uint32_t tiles,
-                                   double* __restrict__ y, uint32_t m) {
+                                   double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest) {
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
   if (base >= tiles) return;
@@ -816,7 +820,7 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
   }
   const bool started_here = (heads >> seg) & 1u;
   const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-  if (tail && lane != 31 && started_here && r < m) y[r] += v;
+  if (tail && lane != 31 && started_here && r < m) put_row<SCATTER>(y, dest, r, y[r] + v);
   // the chunk's last run: finish it here if it started here
   const uint32_t r31 = __shfl_sync(0xFFFFFFFFu, r, 31);
   const bool own31 = __shfl_sync(0xFFFFFFFFu, started_here, 31);
@@ -833,7 +837,7 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
     total += w;
     if (runlen < 32) break;
   }
-  if (lane == 0) y[r31] += total;
+  if (lane == 0) put_row<SCATTER>(y, dest, r31, y[r31] + total);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -860,10 +864,14 @@ void launch_merge_wstage(const Format& f, const double* x, double* y, const Scra
 }
 
 template <int THREADS, int IPT, int NP>
-void launch_merge_vec(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
+void launch_merge_vec(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
+                      const RowDest& dest) {
   constexpr int WARPS = THREADS / 32;
-  merge_spmv_vec_kernel<IPT, WARPS, NP><<<(f.merge_tiles + WARPS - 1) / WARPS, THREADS, 0, s>>>(MERGE_ARGS,
-                                                                                                f.merge_tiles);
+  const unsigned grid = (f.merge_tiles + WARPS - 1) / WARPS;
+  if (dest.n)
+    merge_spmv_vec_kernel<IPT, WARPS, NP, true><<<grid, THREADS, 0, s>>>(MERGE_ARGS, f.merge_tiles, dest);
+  else
+    merge_spmv_vec_kernel<IPT, WARPS, NP, false><<<grid, THREADS, 0, s>>>(MERGE_ARGS, f.merge_tiles, dest);
 }
 
 template <int THREADS, int IPT>
@@ -953,18 +961,31 @@ static const char* merge_kernel_name(int variant) {
 }
 
 template <int T, int I, int V>
-static void launch_merge_shape(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s) {
+static void launch_merge_shape(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
+                               const RowDest& dest) {
   if constexpr (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);
   else if constexpr (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s);
-  else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s);
-  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 1>(f, x, y, sc, s);  // col prefetch
+  else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s, dest);
+  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 1>(f, x, y, sc, s, dest);  // col prefetch
   else if constexpr (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s);
   else launch_merge_tma<T, I, 2>(f, x, y, sc, s);
 }
 
-int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
+int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest_in) {
   if (f.merge_tiles == 0) return kOk;
   const int threads = (int)f.merge_threads, ipt = (int)f.merge_ipt, variant = (int)f.merge_variant;
+  RowDest dest{};
+  if (dest_in) {
+    dest = *dest_in;
+    if (dest.n > kMaxRowDest) {
+      g_last_error = "too many row destinations";
+      return kInvalidArgument;
+    }
+    if (dest.n && variant != kVariantVector && variant != kVariantVector3) {
+      g_last_error = "row scatter needs the vector merge kernel";
+      return kInvalidArgument;
+    }
+  }
   const Scratch* sc = f.stream_scratch(s);
   if (!sc) {
     g_last_error = "device allocation failed (merge carry scratch)";
@@ -974,7 +995,7 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
   timing_begin(merge_kernel_name(variant), s);
 #define SPMV_MERGE_SHAPE(T, I, V)                              \
   if (!launched && threads == T && ipt == I && variant == V) { \
-    launch_merge_shape<T, I, V>(f, x, y, sc, s);               \
+    launch_merge_shape<T, I, V>(f, x, y, sc, s, dest);         \
     launched = true;                                           \
   }
 #include "merge_shapes.inc"
@@ -985,7 +1006,11 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s) {
     return kInvalidArgument;
   }
   note_launch(2);
-  merge_fixup_kernel<<<(f.merge_tiles + 255) / 256, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m);
+  const unsigned fgrid = (f.merge_tiles + 255) / 256;
+  if (dest.n)
+    merge_fixup_kernel<true><<<fgrid, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m, dest);
+  else
+    merge_fixup_kernel<false><<<fgrid, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m, dest);
   return check_launch("spmv_merge");
 }
 

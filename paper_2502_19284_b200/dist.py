@@ -81,3 +81,119 @@ class ShardedSpMV:
             self.step(x, y)
             x, y = y, x
         return x
+
+
+def _device_view(ptr: int, count: int, device) -> torch.Tensor:
+    """A float64 tensor over library-owned device memory (no copy, no ownership)."""
+    class _V:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_V(), device=device)
+
+
+class FusedExchangeSpMV:
+    """Row-sharded iterated merge-CSR with the exchange fused into the multiply (SURVEY §8e,
+    stretch): every rank owns two exchange buffers of the full x (ping-pong) that all ranks map
+    through CUDA IPC; a step multiplies the local rows and the kernel epilogue stores each finished
+    row straight into the next-x buffer of every rank (own rows locally, the others over NVLink /
+    NVSwitch peer stores) -- no separate all-gather pass over y.  A rank barrier ends the step.
+
+    `fmt` is the rank's CRS-family shard format (rows [lo, hi), global columns); `barrier` is a
+    callable (default torch.distributed.barrier on `group`)."""
+
+    def __init__(self, cuts: Sequence[int], rank: int, fmt, n: int, group=None, barrier=None):
+        import ctypes as C
+        import torch.distributed as dist
+        from . import capi
+        from .engine import _check
+        self.C, self.capi, self._check = C, capi, _check
+        L = capi.load()
+        self.cuts = list(cuts)
+        self.rank, self.world = rank, len(cuts) - 1
+        self.lo, self.hi = self.cuts[rank], self.cuts[rank + 1]
+        self.fmt, self.n = fmt, n
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.barrier = barrier or (lambda: dist.barrier(group))
+        self.own, handles, err = [], [], None
+        try:
+            for _ in range(2):
+                p, h = C.c_void_p(), (C.c_ubyte * 64)()
+                _check(L.spmvlab_cuda_exchange_alloc(8 * max(n, 1), C.byref(p), h))
+                self.own.append(p.value)
+                handles.append(bytes(h))
+        except Exception as e:  # agree on failure collectively instead of leaving peers waiting
+            err = repr(e)
+        every = [None] * self.world
+        dist.all_gather_object(every, (err, handles), group)
+        self.opened = []
+        self.ptr = [[0] * self.world for _ in range(2)]  # ptr[buffer][rank], mapped into this process
+        if err is None and all(e is None for e, _ in every):
+            try:
+                for q in range(self.world):
+                    for b in range(2):
+                        if q == rank:
+                            self.ptr[b][q] = self.own[b]
+                            continue
+                        p = C.c_void_p()
+                        _check(L.spmvlab_cuda_exchange_open((C.c_ubyte * 64).from_buffer_copy(every[q][1][b]),
+                                                            C.byref(p)))
+                        self.ptr[b][q] = p.value
+                        self.opened.append(p.value)
+            except Exception as e:
+                err = repr(e)
+        else:
+            err = err or next(e for e, _ in every if e is not None)
+        status = [None] * self.world
+        dist.all_gather_object(status, err, group)
+        failed = [s for s in status if s is not None]
+        if failed:
+            for p in self.opened:
+                L.spmvlab_cuda_exchange_close(p, 1)
+            self.barrier()
+            for p in self.own:
+                L.spmvlab_cuda_exchange_close(p, 0)
+            self.opened, self.own = [], []
+            raise RuntimeError(f"fused exchange unavailable: {failed[0]}")
+        self.cur = 0
+
+    def x(self) -> torch.Tensor:
+        """This rank's copy of the current iterate (a view of the exchange buffer)."""
+        return _device_view(self.ptr[self.cur][self.rank], self.n, self.device)
+
+    def load(self, x0: torch.Tensor) -> None:
+        self.x().copy_(x0)
+        torch.cuda.synchronize()
+        self.barrier()
+
+    def step(self, stream=None) -> None:
+        C = self.C
+        nxt = 1 - self.cur
+        peers = [self.ptr[nxt][q] for q in range(self.world) if q != self.rank]
+        dest = (C.c_void_p * max(len(peers), 1))(*peers)
+        st = stream or torch.cuda.current_stream()
+        y_local = self.ptr[nxt][self.rank] + 8 * self.lo  # own rows go straight into the own next x
+        self._check(self.capi.load().spmvlab_cuda_run_spmv_scatter(
+            self.fmt.handle, self.ptr[self.cur][self.rank], self.n, y_local, self.hi - self.lo, dest, len(peers),
+            self.lo, st.cuda_stream))
+        st.synchronize()
+        self.barrier()  # every rank's rows have landed in every next buffer
+        self.cur = nxt
+
+    def iterate(self, x0: torch.Tensor, iters: int) -> torch.Tensor:
+        self.load(x0)
+        for _ in range(iters):
+            self.step()
+        return self.x().clone()
+
+    def close(self) -> None:
+        """Collective: unmaps the peers' buffers, then (after every rank did) frees its own."""
+        L = self.capi.load()
+        torch.cuda.synchronize()
+        self.barrier()
+        for p in self.opened:
+            L.spmvlab_cuda_exchange_close(p, 1)
+        self.barrier()
+        for p in self.own:
+            L.spmvlab_cuda_exchange_close(p, 0)
+        self.opened, self.own = [], []
