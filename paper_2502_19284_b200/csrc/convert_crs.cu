@@ -164,20 +164,41 @@ int build_merge_plan(Format& f, Arena& ar) {
   if (!f.stream_scratch(s)) return kNoMemory;
   merge_partition<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, s>>>(
       f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, tile_items, trow, tnnz);
-  // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32].
+  // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32]; rows longer
+  // than kParLongIters * width get one CTA each.  On heavy-tailed row lengths (more than 0.1 % of
+  // the rows are "long") many narrow groups plus the per-row CTAs win instead: width 2, CTAs above
+  // 64 nonzeros (R-MAT s22: 1061 -> 492 us; uniform ER / Laplacian rows keep the mean rule).
   const double mean = f.m ? (double)f.nnz / f.m : 0.0;
   uint32_t g = 2;
   while (g < 32 && g < mean) g <<= 1;
-  f.par_group = g;
-  // ParCRS long rows (> kParLongIters * g nonzeros) get one CTA each; the rest stay with the groups.
-  const uint32_t lim = kParLongIters * g;
+  uint32_t lim = kParLongIters * g;
+  const char* eg = getenv("SPMVLAB_PARCRS_G");  // developer overrides
+  const char* el = getenv("SPMVLAB_PARCRS_LIM");
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)f.m + 1);
   if (!flag) return kNoMemory;
-  if (f.m) long_row_flags<<<(f.m + 255) / 256, 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, lim, flag);
-  exclusive_scan_u32(flag, flag, f.m, ar);
   uint32_t nlong = 0;
-  cudaMemcpyAsync(&nlong, flag + f.m, 4, cudaMemcpyDeviceToHost, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan");
+  auto count_long = [&](uint32_t l) -> int {
+    if (f.m) long_row_flags<<<(f.m + 255) / 256, 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, l, flag);
+    exclusive_scan_u32(flag, flag, f.m, ar);
+    cudaMemcpyAsync(&nlong, flag + f.m, 4, cudaMemcpyDeviceToHost, s);
+    return cudaStreamSynchronize(s) != cudaSuccess ? check_launch("build_merge_plan") : kOk;
+  };
+  if (int rc = count_long(lim)) return rc;
+  if (!eg && !el && (uint64_t)nlong * 1000 > f.m && g > 2) {
+    g = 2;
+    lim = 2 * kParLongIters;
+    if (int rc = count_long(lim)) return rc;
+  }
+  if (eg || el) {
+    if (eg) {
+      const int v = atoi(eg);
+      if (v == 2 || v == 4 || v == 8 || v == 16 || v == 32) g = (uint32_t)v;
+    }
+    lim = el ? (uint32_t)std::max(1, atoi(el)) : kParLongIters * g;
+    if (int rc = count_long(lim)) return rc;
+  }
+  f.par_group = g;
+  f.par_lim = lim;
   uint32_t* lr = static_cast<uint32_t*>(f.add("par_long_rows", nlong, 4, s));
   if (nlong && !lr) return kNoMemory;
   if (nlong)

@@ -41,7 +41,8 @@ struct spmvlab_cuda_format {
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;
-  uint32_t par_long = 0;  // ParCRS rows with > kParLongRow nonzeros ("par_long_rows")
+  uint32_t par_long = 0;  // rows with > par_lim nonzeros ("par_long_rows", one CTA each)
+  uint32_t par_lim = 0xFFFFFFFFu;
 
   // ---- blocked plan (CSB / MergeB / BCOH): work items = (element range, y window)
   uint32_t work_items = 0;

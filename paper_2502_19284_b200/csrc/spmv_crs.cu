@@ -4,7 +4,8 @@
 //    explicitly rounded multiply and add (no FMA contraction), so y is BITWISE equal to the
 //    reference's sequential kernel.
 //  * ParCrs (spmv_parcrs, inc/spmv_parallel.hpp:106-125): rows claimed by sub-warp groups whose
-//    width is the next power of two >= the mean row length; lanes stride the row, shuffle-reduce.
+//    width is the next power of two >= the mean row length (2 on heavy-tailed row lengths); lanes
+//    stride the row, shuffle-reduce; rows above a length threshold get one CTA each.
 //  * Merge (spmv_merge, inc/spmv_parallel.hpp:130-160): the merge path over (row_ptr[1..m],
 //    0..nnz-1) is cut into equal tiles at build time (merge_partition: one diagonal search per
 //    tile boundary, spmv_parallel.hpp:47-86).  Each tile leaves one (row, partial) carry-out and a
@@ -903,7 +904,7 @@ int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.m == 0) return kOk;
   const DevArray* lra = f.find("par_long_rows");
   const uint32_t* lr = lra ? lra->as<uint32_t>() : nullptr;
-  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? kParLongIters * f.par_group : 0xFFFFFFFFu;
+  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? f.par_lim : 0xFFFFFFFFu;
   timing_begin("seq_crs_kernel", s);
   seq_crs_kernel<<<(f.m + kSeqThreads - 1) / kSeqThreads + nl, kSeqThreads, 0, s>>>(
       f.find("row_ptr")->as<uint32_t>(), f.find("col_ind")->as<uint32_t>(), f.find("data")->as<double>(), x, y,
@@ -921,7 +922,7 @@ int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   const unsigned blocks = grid_for((uint64_t)f.m * f.par_group, 256, kNumSMs * 8) + f.par_long;
   const DevArray* lra = f.find("par_long_rows");
   const uint32_t* lr = lra ? lra->as<uint32_t>() : nullptr;
-  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? kParLongIters * f.par_group : 0xFFFFFFFFu;
+  const uint32_t nl = lr ? f.par_long : 0, lim = lr ? f.par_lim : 0xFFFFFFFFu;
   note_launch();
   timing_begin("par_crs_kernel", s);
   switch (f.par_group) {
