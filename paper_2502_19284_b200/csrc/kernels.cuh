@@ -49,7 +49,11 @@ struct RowDest {
 // kernels keep their register / stack budget); kernels take the list as __grid_constant__.
 template <bool SCATTER>
 __device__ __forceinline__ void put_row(double* y, const RowDest& d, uint32_t r, double v) {
-  y[r] = v;
+  {  // y is written once: evict-first keeps the L2 for x (cfg3 / cfg4, x ~ L2 size: -2..3 %)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(y + r), "d"(v), "l"(pol) : "memory");
+  }
   if constexpr (SCATTER)
     for (unsigned i = 0; i < d.n; ++i) d.p[i][d.off + r] = v;
 }
