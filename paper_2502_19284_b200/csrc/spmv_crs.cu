@@ -665,6 +665,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge
   *reinterpret_cast<int4*>(smap + 4 * lane) = make_int4(-1, -1, -1, -1);
   const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
+  // (a fractional evict-last share for x larger than the L2 measured within 1 % on cfg3-5)
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   uint32_t rp = r0;
   uint32_t prevE = __ldg(row_ptr + r0);
