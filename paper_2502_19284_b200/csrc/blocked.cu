@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(256) blocked_spmv_kernel(
       // warp segmented sum over runs of equal rows
       const uint32_t prow = __shfl_up_sync(0xFFFFFFFFu, row, 1);
       const unsigned heads = __ballot_sync(0xFFFFFFFFu, lane == 0 || prow != row);
+      // (skipping the scan when every lane is its own row measured slower for the packed formats)
       const int seg_start = 31 - __clz(heads & (lt | (1u << lane)));
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
