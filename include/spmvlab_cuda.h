@@ -235,6 +235,26 @@ int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, u
 
 void spmvlab_cuda_free_bicrs(spmvlab_cuda_bicrs* a);
 
+/* --- CSB work items (inc/spmv_parallel.hpp:167-264) ------------------------------------------ */
+
+/* CsbWorkItem (spmv_parallel.hpp:167-174): cells [cell_begin, cell_end) of block_row clipped to
+ * elements [elem_begin, elem_end); temp_slot -1 = the item owns its block row. */
+typedef struct {
+  uint32_t block_row, cell_begin, cell_end;
+  int32_t temp_slot;
+  uint64_t elem_begin, elem_end;
+} spmvlab_cuda_csb_item;
+
+/* The work-item list spmv_csb builds (spmv_parallel.hpp:202-264: per block row one item, or
+ * greedy cell chunks plus the quadrant leaves of split_block_range :178-193 for cells above the
+ * threshold), built on the device and bit-identical to the reference's, in the reference's order.
+ * Algorithms 3 (csb) and 4 (csbh) only (else InvalidArgument).  split_threshold 0 = 2 * beta.
+ * *count receives the list length; items (device, may be NULL to only count) must hold
+ * `capacity` >= *count entries, else InvalidArgument.  Synchronises `stream`. */
+int spmvlab_cuda_csb_work_items(const spmvlab_cuda_format* f, uint64_t split_threshold,
+                                spmvlab_cuda_csb_item* items, uint64_t capacity, uint64_t* count,
+                                void* stream);
+
 /* --- primitives, exposed for parity tests ---------------------------------------------------- */
 
 /* select_block_size -- inc/block_size.hpp:47-61 (value_size 8). Host computation. */

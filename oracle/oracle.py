@@ -25,6 +25,9 @@ ALGORITHMS = ["crs", "parcrs", "merge", "csb", "csbh", "bcoh", "bcohc", "bcohch"
               "mergeb", "mergebh"]
 
 _DT = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}
+# CsbWorkItem (inc/spmv_parallel.hpp:167-174) as orc_csb_item / spmvlab_cuda_csb_item
+CSB_ITEM_DTYPE = np.dtype([("block_row", np.uint32), ("cell_begin", np.uint32), ("cell_end", np.uint32),
+                           ("temp_slot", np.int32), ("elem_begin", np.uint64), ("elem_end", np.uint64)])
 _SIGNED = {"row_jump_block": np.int16, "col_jump_block": np.int16, "data": np.float64}
 
 
@@ -136,6 +139,8 @@ class Oracle:
         L.orc_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_csb_work_items.argtypes = [C.POINTER(OrcFormat), C.c_uint64, C.c_void_p, C.c_uint64,
+                                         C.POINTER(C.c_uint64)]
 
     # -- formats ----------------------------------------------------------------------------
     def build(self, alg: int, m: int, n: int, rows, cols, vals, threads: int = 1,
@@ -152,10 +157,9 @@ class Oracle:
             self.lib.orc_free_format(fp)
         return Built(meta, arrays, storage, handle=None)
 
-    def spmv(self, built: Built, alg: int, x, p: int = 1, split_threshold: int = 0):
-        """Rebuilds the C struct from the numpy arrays and replays the reference kernel."""
-        x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.zeros(built.meta["m"], dtype=np.float64)
+    @staticmethod
+    def _struct(built: Built):
+        """The C struct over the numpy arrays (returned with the arrays it points into)."""
         f = OrcFormat()
         for k, v in built.meta.items():
             setattr(f, k, v)
@@ -170,11 +174,32 @@ class Oracle:
             f.arrays[i].data = a.ctypes.data if a.size else None
             f.arrays[i].bytes = a.nbytes
             f.arrays[i].elem_size = a.itemsize
+        return f, keep
+
+    def spmv(self, built: Built, alg: int, x, p: int = 1, split_threshold: int = 0):
+        """Rebuilds the C struct from the numpy arrays and replays the reference kernel."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(built.meta["m"], dtype=np.float64)
+        f, keep = self._struct(built)
         rc = self.lib.orc_run_spmv(alg, C.byref(f), _p(x, C.c_double), len(x), _p(y, C.c_double),
                                    len(y), p, split_threshold)
         if rc:
             raise CheckerError(rc, "orc_run_spmv")
         return y
+
+    def csb_work_items(self, built: Built, split_threshold: int = 0) -> np.ndarray:
+        """spmv_csb's work-item list (structured array, CSB_ITEM_DTYPE)."""
+        f, keep = self._struct(built)
+        cnt = C.c_uint64()
+        rc = self.lib.orc_csb_work_items(C.byref(f), split_threshold, None, 0, C.byref(cnt))
+        if rc:
+            raise CheckerError(rc, "orc_csb_work_items")
+        out = np.zeros(cnt.value, dtype=CSB_ITEM_DTYPE)
+        rc = self.lib.orc_csb_work_items(C.byref(f), split_threshold, out.ctypes.data_as(C.c_void_p),
+                                         len(out), C.byref(cnt))
+        if rc:
+            raise CheckerError(rc, "orc_csb_work_items")
+        return out
 
     # -- primitives -------------------------------------------------------------------------
     def spmv_triplet(self, m, rows, cols, vals, x):
@@ -322,6 +347,8 @@ class Reference:
         L.ref_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.ref_free_buf.argtypes = [C.c_void_p]
+        L.ref_csb_leaves.restype = C.c_int64
+        L.ref_csb_leaves.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64]
 
     def cache_read(self, path):
         return _cache_read(self.lib.ref_cache_read, self.lib.ref_free_buf, path)
@@ -374,6 +401,15 @@ class Reference:
 
     def storage_total(self, built: Built) -> int:
         return int(self.lib.ref_storage_total(built.handle.h))
+
+    def csb_leaves(self, built: Built, threshold: int) -> np.ndarray:
+        """detail::split_block_range's leaves of every cell above `threshold`: rows (cell, lo, hi)."""
+        cap = max(16, built.meta["nnz"] + 1)
+        out = np.zeros(3 * cap, dtype=np.uint64)
+        k = self.lib.ref_csb_leaves(built.handle.h, threshold, _p(out, C.c_uint64), cap)
+        if k < 0:
+            raise CheckerError(2, f"ref_csb_leaves: {k}")
+        return out[: 3 * k].reshape(k, 3)
 
     def select_block_size(self, n, cap, l2=512 * 1024):
         return int(self.lib.ref_select_block_size(n, cap, l2))

@@ -265,4 +265,31 @@ void ref_verification_input(uint32_t n, uint64_t seed, double* x) {
 }
 unsigned ref_hardware_threads() { return hardware_threads(); }
 
+// The reference's own quadrant leaves (detail::split_block_range, spmv_parallel.hpp:178-193) of
+// every cell holding more than `threshold` elements of a built CSB format, cells ascending:
+// out[3k..3k+2] = (cell, first element, end element).  Returns the leaf count (-1: not CSB;
+// -2: capacity too small).
+int64_t ref_csb_leaves(void* hv, uint64_t threshold, uint64_t* out, uint64_t capacity) {
+  auto* h = static_cast<Handle*>(hv);
+  const auto* a = std::get_if<CsbMatrix>(&h->fmt);
+  if (!a) return -1;
+  uint64_t k = 0;
+  const uint64_t cells = static_cast<uint64_t>(a->block_rows) * a->block_cols;
+  std::vector<std::pair<std::size_t, std::size_t>> leaves;
+  for (uint64_t cell = 0; cell < cells; ++cell) {
+    if (a->blk_ptr[cell + 1] - a->blk_ptr[cell] <= threshold) continue;
+    leaves.clear();
+    detail::split_block_range(*a, a->blk_ptr[cell], a->blk_ptr[cell + 1], a->beta.beta, {},
+                              threshold, leaves);
+    for (const auto& [lo, hi] : leaves) {
+      if (k >= capacity) return -2;
+      out[3 * k] = cell;
+      out[3 * k + 1] = lo;
+      out[3 * k + 2] = hi;
+      ++k;
+    }
+  }
+  return static_cast<int64_t>(k);
+}
+
 }  // extern "C"

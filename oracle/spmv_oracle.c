@@ -835,30 +835,16 @@ static void split_block_range(const uint32_t* packed, int hilbert, uint64_t begi
                       hilbert ? hil_child(st, pos) : st, threshold, leaves, nleaves);
 }
 
-typedef struct {
-  uint32_t block_row, cell_begin, cell_end;
-  uint64_t elem_begin, elem_end;
-  int64_t temp_slot;
-} csb_item;
-
-/* spmv_csb, spmv_parallel.hpp:202-331: work items, temp slots, pairwise slot reduction.  The
- * result is independent of p (deterministic reduction order), so it is replayed sequentially. */
-static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t split_threshold) {
+/* The work-item list of spmv_csb, spmv_parallel.hpp:209-264.  Returns the number of items; items
+ * must hold nnz + block_rows * (block_cols + 1) entries (an upper bound). */
+static uint64_t csb_items(const orc_format* f, uint64_t threshold, orc_csb_item* items) {
   const uint32_t* blk_ptr = ARR(f, "blk_ptr", uint32_t);
   const uint32_t* packed = ARR(f, "packed", uint32_t);
-  const double* d = ARR(f, "data", double);
-  const unsigned lb = f->log2_beta;
-  const uint32_t beta = UINT32_C(1) << lb;
+  const uint32_t beta = UINT32_C(1) << f->log2_beta;
   const int hilbert = f->alg == ORC_CSBH;
-  const uint64_t threshold = split_threshold == 0 ? 2 * (uint64_t)beta : split_threshold;
   const uint32_t bcs = f->block_cols;
-
-  uint64_t cap = (uint64_t)f->nnz + (uint64_t)f->block_rows * (bcs + 1) + 16;
-  csb_item* items = (csb_item*)malloc(sizeof(csb_item) * cap);
   uint64_t nitems = 0;
-  typedef struct { uint32_t block_row; uint64_t slot_begin, slot_count; } split_row;
-  split_row* srows = (split_row*)malloc(sizeof(split_row) * (f->block_rows + 1));
-  uint64_t nsrows = 0, total_slots = 0;
+  int32_t slot = 0;
   range64* leaves = (range64*)malloc(sizeof(range64) * ((uint64_t)f->nnz + 1));
 
   for (uint32_t br = 0; br < f->block_rows; ++br) {
@@ -866,19 +852,17 @@ static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t s
     const uint64_t rb = blk_ptr[row_cell], re = blk_ptr[row_cell + bcs];
     if (re == rb) continue;
     if (re - rb <= threshold) {
-      csb_item t = {br, 0, bcs, rb, re, -1};
+      orc_csb_item t = {br, 0, bcs, -1, rb, re};
       items[nitems++] = t;
       continue;
     }
-    const uint64_t slot_begin = total_slots;
-    int64_t slot = (int64_t)total_slots;
     uint32_t chunk_first = 0;
     uint64_t chunk_count = 0;
 #define FLUSH_CHUNK(cell_end)                                                          \
   do {                                                                                 \
     if (chunk_count != 0) {                                                            \
-      csb_item t = {br, chunk_first, (cell_end), blk_ptr[row_cell + chunk_first],      \
-                    blk_ptr[row_cell + (cell_end)], slot++};                           \
+      orc_csb_item t = {br, chunk_first, (cell_end), slot++,                           \
+                        blk_ptr[row_cell + chunk_first], blk_ptr[row_cell + (cell_end)]}; \
       items[nitems++] = t;                                                             \
       chunk_count = 0;                                                                 \
     }                                                                                  \
@@ -891,7 +875,7 @@ static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t s
         split_block_range(packed, hilbert, blk_ptr[row_cell + c], blk_ptr[row_cell + c + 1], beta,
                           0, threshold, leaves, &nl);
         for (uint64_t l = 0; l < nl; ++l) {
-          csb_item t = {br, c, c + 1, leaves[l].lo, leaves[l].hi, slot++};
+          orc_csb_item t = {br, c, c + 1, slot++, leaves[l].lo, leaves[l].hi};
           items[nitems++] = t;
         }
         chunk_first = c + 1;
@@ -906,13 +890,58 @@ static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t s
     }
     FLUSH_CHUNK(bcs);
 #undef FLUSH_CHUNK
-    srows[nsrows].block_row = br;
-    srows[nsrows].slot_begin = slot_begin;
-    srows[nsrows].slot_count = (uint64_t)slot - slot_begin;
-    ++nsrows;
-    total_slots = (uint64_t)slot;
   }
   free(leaves);
+  return nitems;
+}
+
+int orc_csb_work_items(const orc_format* f, uint64_t split_threshold, orc_csb_item* items,
+                       uint64_t capacity, uint64_t* count) {
+  if (f->alg != ORC_CSB && f->alg != ORC_CSBH) return ORC_INVALID_ARGUMENT;
+  const uint64_t threshold = split_threshold == 0 ? 2 * ((uint64_t)1 << f->log2_beta) : split_threshold;
+  const uint64_t cap = (uint64_t)f->nnz + (uint64_t)f->block_rows * (f->block_cols + 1) + 16;
+  orc_csb_item* all = (orc_csb_item*)malloc(sizeof(orc_csb_item) * cap);
+  if (!all) return ORC_NO_MEMORY;
+  const uint64_t n = csb_items(f, threshold, all);
+  *count = n;
+  int rc = ORC_OK;
+  if (items) {
+    if (capacity < n) rc = ORC_INVALID_ARGUMENT;
+    else memcpy(items, all, sizeof(orc_csb_item) * n);
+  }
+  free(all);
+  return rc;
+}
+
+/* spmv_csb, spmv_parallel.hpp:202-331: work items, temp slots, pairwise slot reduction.  The
+ * result is independent of p (deterministic reduction order), so it is replayed sequentially. */
+static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t split_threshold) {
+  const uint32_t* blk_ptr = ARR(f, "blk_ptr", uint32_t);
+  const uint32_t* packed = ARR(f, "packed", uint32_t);
+  const double* d = ARR(f, "data", double);
+  const unsigned lb = f->log2_beta;
+  const uint32_t beta = UINT32_C(1) << lb;
+  const uint64_t threshold = split_threshold == 0 ? 2 * (uint64_t)beta : split_threshold;
+  const uint32_t bcs = f->block_cols;
+
+  uint64_t cap = (uint64_t)f->nnz + (uint64_t)f->block_rows * (bcs + 1) + 16;
+  orc_csb_item* items = (orc_csb_item*)malloc(sizeof(orc_csb_item) * cap);
+  const uint64_t nitems = csb_items(f, threshold, items);
+  /* split rows: consecutive items with slots, in block-row order */
+  typedef struct { uint32_t block_row; uint64_t slot_begin, slot_count; } split_row;
+  split_row* srows = (split_row*)malloc(sizeof(split_row) * (f->block_rows + 1));
+  uint64_t nsrows = 0, total_slots = 0;
+  for (uint64_t t = 0; t < nitems; ++t) {
+    if (items[t].temp_slot < 0) continue;
+    if (nsrows == 0 || srows[nsrows - 1].block_row != items[t].block_row) {
+      srows[nsrows].block_row = items[t].block_row;
+      srows[nsrows].slot_begin = (uint64_t)items[t].temp_slot;
+      srows[nsrows].slot_count = 0;
+      ++nsrows;
+    }
+    ++srows[nsrows - 1].slot_count;
+    ++total_slots;
+  }
 
   double** temps = (double**)calloc(total_slots ? total_slots : 1, sizeof(double*));
   for (uint64_t r = 0; r < nsrows; ++r) {
@@ -923,7 +952,7 @@ static void spmv_csb(const orc_format* f, const double* x, double* y, uint64_t s
   }
   for (uint32_t i = 0; i < f->m; ++i) y[i] = 0.0;
   for (uint64_t t = 0; t < nitems; ++t) {
-    const csb_item* it = &items[t];
+    const orc_csb_item* it = &items[t];
     double* target = it->temp_slot < 0 ? y + ((uint64_t)it->block_row << lb) : temps[it->temp_slot];
     const uint64_t row_cell = (uint64_t)it->block_row * bcs;
     for (uint32_t c = it->cell_begin; c < it->cell_end; ++c) {

@@ -8,6 +8,7 @@ from .engine import (  # noqa: F401
     algorithm_from_name, algorithm_name, all_algorithms, build_format, cache_read, cache_write, curve_keys,
     MatrixHeader, load_matrix, read_matrix_market, read_matrix_market_host,
     IncrementalRowStorage, bicrs_from_arrays, crs_to_icrs, triplet_to_bicrs,
+    CSB_ITEM_DTYPE, csb_items_numpy, csb_work_items,
     engine_block_size, exclusive_scan, iterate, merge_path_search, partition_rows_by_nnz, run_spmv,
     run_spmv_host, select_block_size, sort_pairs, storage_report, validate,
 )

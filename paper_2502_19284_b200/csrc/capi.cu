@@ -570,6 +570,15 @@ int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, u
   return bicrs_decode_all(*a, rows, cols, nullptr, static_cast<cudaStream_t>(stream));
 }
 
+int spmvlab_cuda_csb_work_items(const spmvlab_cuda_format* f, uint64_t split_threshold,
+                                spmvlab_cuda_csb_item* items, uint64_t capacity, uint64_t* count,
+                                void* stream) {
+  if (!f || !count) return fail(kInvalidArgument, "null argument");
+  if (f->alg != 3 && f->alg != 4) return fail(kInvalidArgument, "format is not CSB");
+  g_last_error.clear();
+  return csb_work_items(*f, split_threshold, items, capacity, count, static_cast<cudaStream_t>(stream));
+}
+
 void spmvlab_cuda_free_bicrs(spmvlab_cuda_bicrs* a) {
   if (!a) return;
   cudaFree(a->col_inc);

@@ -466,6 +466,28 @@ def crs_to_icrs(fmt: BuiltFormat, stream=None) -> IncrementalRowStorage:
     return IncrementalRowStorage(c)
 
 
+CSB_ITEM_DTYPE = np.dtype([("block_row", np.uint32), ("cell_begin", np.uint32), ("cell_end", np.uint32),
+                           ("temp_slot", np.int32), ("elem_begin", np.uint64), ("elem_end", np.uint64)])
+
+
+def csb_work_items(fmt: BuiltFormat, split_threshold: int = 0, stream=None) -> torch.Tensor:
+    """spmv_csb's work-item list (inc/spmv_parallel.hpp:202-264: CsbWorkItem per block row, cell
+    chunk or quadrant leaf of split_block_range :178-193), built on the device from a CSB / CSBH
+    format; split_threshold 0 = 2 * beta.  Returns a device uint8 tensor of shape (count, 32) in
+    the spmvlab_cuda_csb_item layout; csb_items_numpy() views a host copy as CSB_ITEM_DTYPE."""
+    L = capi.load()
+    cnt = C.c_uint64()
+    _check(L.spmvlab_cuda_csb_work_items(fmt.handle, split_threshold, None, 0, C.byref(cnt), _stream(stream)))
+    out = torch.empty((cnt.value, CSB_ITEM_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    _check(L.spmvlab_cuda_csb_work_items(fmt.handle, split_threshold, out.data_ptr() if cnt.value else None,
+                                         cnt.value, C.byref(cnt), _stream(stream)))
+    return out
+
+
+def csb_items_numpy(items: torch.Tensor) -> np.ndarray:
+    return items.cpu().numpy().reshape(-1).view(CSB_ITEM_DTYPE)
+
+
 def triplet_to_bicrs(a: TripletMatrix, order: torch.Tensor, stream=None) -> IncrementalRowStorage:
     """triplet_to_bicrs (inc/bicrs.hpp:154-200) with the elements in `order` (device int32)."""
     c = capi.Bicrs()
