@@ -235,6 +235,15 @@ int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, u
 
 void spmvlab_cuda_free_bicrs(spmvlab_cuda_bicrs* a);
 
+/* --- format -> triplet ------------------------------------------------------------------------ */
+
+/* crs_to_triplet (crs.hpp:94-105), csb_to_triplet (csb.hpp:103-120), mergeb_to_triplet
+ * (mergeb.hpp:110-127), bcoh_to_triplet (bcoh.hpp:379-392) for any built format: the row, column
+ * and value (vals may be NULL) of every element in the reference's output order (storage order;
+ * BCOH band by band), into device arrays of nnz entries.  Stream-ordered. */
+int spmvlab_cuda_format_to_triplet(const spmvlab_cuda_format* f, uint32_t* rows, uint32_t* cols, double* vals,
+                                   void* stream);
+
 /* --- CSB work items (inc/spmv_parallel.hpp:167-264) ------------------------------------------ */
 
 /* CsbWorkItem (spmv_parallel.hpp:167-174): cells [cell_begin, cell_end) of block_row clipped to

@@ -139,6 +139,8 @@ class Oracle:
         L.orc_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_format_to_triplet.argtypes = [C.POINTER(OrcFormat), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                            C.POINTER(C.c_double)]
         L.orc_csb_work_items.argtypes = [C.POINTER(OrcFormat), C.c_uint64, C.c_void_p, C.c_uint64,
                                          C.POINTER(C.c_uint64)]
 
@@ -186,6 +188,16 @@ class Oracle:
         if rc:
             raise CheckerError(rc, "orc_run_spmv")
         return y
+
+    def to_triplet(self, built: Built):
+        """orc_format_to_triplet: (rows, cols, vals) in storage order."""
+        f, keep = self._struct(built)
+        nnz = built.meta["nnz"]
+        r, c, v = np.zeros(nnz, np.uint32), np.zeros(nnz, np.uint32), np.zeros(nnz)
+        rc = self.lib.orc_format_to_triplet(C.byref(f), _p(r, C.c_uint32), _p(c, C.c_uint32), _p(v, C.c_double))
+        if rc:
+            raise CheckerError(rc, "orc_format_to_triplet")
+        return r, c, v
 
     def csb_work_items(self, built: Built, split_threshold: int = 0) -> np.ndarray:
         """spmv_csb's work-item list (structured array, CSB_ITEM_DTYPE)."""
@@ -347,6 +359,8 @@ class Reference:
         L.ref_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.ref_free_buf.argtypes = [C.c_void_p]
+        L.ref_to_triplet.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_double)]
         L.ref_csb_leaves.restype = C.c_int64
         L.ref_csb_leaves.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64]
 
@@ -401,6 +415,15 @@ class Reference:
 
     def storage_total(self, built: Built) -> int:
         return int(self.lib.ref_storage_total(built.handle.h))
+
+    def to_triplet(self, built: Built):
+        """crs_/csb_/mergeb_/bcoh_to_triplet: (rows, cols, vals) in the reference's order."""
+        nnz = built.meta["nnz"]
+        r, c, v = np.zeros(nnz, np.uint32), np.zeros(nnz, np.uint32), np.zeros(nnz)
+        rc = self.lib.ref_to_triplet(built.handle.h, _p(r, C.c_uint32), _p(c, C.c_uint32), _p(v, C.c_double))
+        if rc:
+            self._err(rc, "ref_to_triplet")
+        return r, c, v
 
     def csb_leaves(self, built: Built, threshold: int) -> np.ndarray:
         """detail::split_block_range's leaves of every cell above `threshold`: rows (cell, lo, hi)."""

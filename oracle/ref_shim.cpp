@@ -265,6 +265,26 @@ void ref_verification_input(uint32_t n, uint64_t seed, double* x) {
 }
 unsigned ref_hardware_threads() { return hardware_threads(); }
 
+// The reference's *_to_triplet of a built format (crs.hpp:94, csb.hpp:103, mergeb.hpp:110,
+// bcoh.hpp:379): nnz coordinates and values in its output order.
+int ref_to_triplet(void* hv, uint32_t* rows, uint32_t* cols, double* vals) {
+  try {
+    auto* h = static_cast<Handle*>(hv);
+    TripletMatrix t;
+    if (auto* c = std::get_if<CrsMatrix>(&h->fmt)) t = crs_to_triplet(*c);
+    else if (auto* c = std::get_if<CsbMatrix>(&h->fmt)) t = csb_to_triplet(*c);
+    else if (auto* c = std::get_if<MergeBlockMatrix>(&h->fmt)) t = mergeb_to_triplet(*c);
+    else t = bcoh_to_triplet(std::get<BcohMatrix>(h->fmt));
+    std::memcpy(rows, t.row_ind.data(), t.row_ind.size() * sizeof(uint32_t));
+    std::memcpy(cols, t.col_ind.data(), t.col_ind.size() * sizeof(uint32_t));
+    std::memcpy(vals, t.data.data(), t.data.size() * sizeof(double));
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
 // The reference's own quadrant leaves (detail::split_block_range, spmv_parallel.hpp:178-193) of
 // every cell holding more than `threshold` elements of a built CSB format, cells ascending:
 // out[3k..3k+2] = (cell, first element, end element).  Returns the leaf count (-1: not CSB;

@@ -994,7 +994,19 @@ typedef struct {
   uint64_t cell;
   uint64_t rj;
   int err;
+  uint32_t* rows; /* decode mode (bcoh_to_triplet): coordinates at storage positions, no multiply */
+  uint32_t* cols;
 } bcoh_ctx;
+
+/* one element of the band replay: y += a * x, or record its coordinates */
+static void bcoh_visit(bcoh_ctx* c, uint64_t e0, uint64_t k, uint64_t row, uint64_t col, const double* d) {
+  if (c->rows) {
+    c->rows[e0 + k] = (uint32_t)row;
+    c->cols[e0 + k] = (uint32_t)col;
+  } else {
+    c->y[row] += d[k] * c->x[col];
+  }
+}
 
 static void bcoh_block(bcoh_ctx* c, uint32_t br, uint32_t bc, uint64_t begin, uint64_t count) {
   const orc_format* f = c->f;
@@ -1006,17 +1018,17 @@ static void bcoh_block(bcoh_ctx* c, uint32_t br, uint32_t bc, uint64_t begin, ui
   if (f->alg != ORC_BCOH) {
     const uint32_t* pk = ARR(f, "packed", uint32_t) + e0;
     for (uint64_t k = begin; k < begin + count; ++k)
-      c->y[row_base + (pk[k] >> 16)] += d[k] * c->x[col_base + (pk[k] & 0xFFFFu)];
+      bcoh_visit(c, e0, k, row_base + (pk[k] >> 16), col_base + (pk[k] & 0xFFFFu), d);
   } else {
     const uint16_t* ci = ARR(f, "col_inc", uint16_t) + e0;
     const uint16_t* rj = ARR(f, "row_jump", uint16_t) + ARR(f, "off_row_jump", uint64_t)[c->band];
     uint32_t in_col = ci[begin];
     uint32_t in_row = rj[c->rj++];
-    c->y[row_base + in_row] += d[begin] * c->x[col_base + in_col];
+    bcoh_visit(c, e0, begin, row_base + in_row, col_base + in_col, d);
     for (uint64_t k = begin + 1; k < begin + count; ++k) {
       in_col += ci[k];
       if (in_col >= beta) { in_col -= beta; in_row += rj[c->rj++]; }
-      c->y[row_base + in_row] += d[k] * c->x[col_base + in_col];
+      bcoh_visit(c, e0, k, row_base + in_row, col_base + in_col, d);
     }
   }
 }
@@ -1029,15 +1041,18 @@ static void bcoh_walk_fn(void* vctx, uint32_t br, uint32_t bc) {
   if (end > begin) bcoh_block(c, br, bc, begin, end - begin);
 }
 
-static int spmv_bcoh(const orc_format* f, const double* x, double* y, unsigned p) {
+/* Replays every band; y == NULL: decode mode into rows / cols (bcoh_to_triplet, bcoh.hpp:379-392). */
+static int bcoh_replay(const orc_format* f, const double* x, double* y, unsigned p, uint32_t* rows,
+                       uint32_t* cols) {
   if (p != f->bands) return ORC_INVALID_ARGUMENT; /* spmv_parallel.hpp:339-341 */
   for (unsigned b = 0; b < p; ++b) {
     const uint32_t first_row = ARR(f, "band_first_row", uint32_t)[b];
     const uint32_t row_count = ARR(f, "band_row_count", uint32_t)[b];
     const uint32_t fbr = ARR(f, "band_first_block_row", uint32_t)[b];
     const uint32_t nbr = ARR(f, "band_block_row_count", uint32_t)[b];
-    for (uint32_t i = first_row; i < first_row + row_count; ++i) y[i] = 0.0;
-    bcoh_ctx c = {f, b, x, y, 0, 0, 0};
+    if (y)
+      for (uint32_t i = first_row; i < first_row + row_count; ++i) y[i] = 0.0;
+    bcoh_ctx c = {f, b, x, y, 0, 0, 0, y ? NULL : rows, y ? NULL : cols};
     if (f->alg != ORC_BCOHCHP) {
       const uint64_t b0 = ARR(f, "off_block", uint64_t)[b], b1 = ARR(f, "off_block", uint64_t)[b + 1];
       const uint32_t* bn = ARR(f, "block_nnz", uint32_t) + b0;
@@ -1062,6 +1077,48 @@ static int spmv_bcoh(const orc_format* f, const double* x, double* y, unsigned p
     } else {
       hilbert_rect_walk(f->block_level, fbr, fbr + nbr, 0, f->block_cols, bcoh_walk_fn, &c);
     }
+  }
+  return ORC_OK;
+}
+
+static int spmv_bcoh(const orc_format* f, const double* x, double* y, unsigned p) {
+  return bcoh_replay(f, x, y, p, NULL, NULL);
+}
+
+/* crs_to_triplet (crs.hpp:94-105), csb_to_triplet (csb.hpp:103-120), mergeb_to_triplet
+ * (mergeb.hpp:110-127), bcoh_to_triplet (bcoh.hpp:379-392): coordinates in storage order. */
+int orc_format_to_triplet(const orc_format* f, uint32_t* rows, uint32_t* cols, double* vals) {
+  const unsigned lb = f->log2_beta;
+  if (vals && f->nnz) memcpy(vals, ARR(f, "data", double), sizeof(double) * f->nnz);
+  if (f->alg <= ORC_MERGE) {
+    const uint32_t* rp = ARR(f, "row_ptr", uint32_t);
+    if (f->nnz) memcpy(cols, ARR(f, "col_ind", uint32_t), sizeof(uint32_t) * f->nnz);
+    for (uint32_t i = 0; i < f->m; ++i)
+      for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) rows[k] = i;
+  } else if (f->alg == ORC_CSB || f->alg == ORC_CSBH) {
+    const uint32_t* bp = ARR(f, "blk_ptr", uint32_t);
+    const uint32_t* pk = ARR(f, "packed", uint32_t);
+    for (uint32_t br = 0; br < f->block_rows; ++br)
+      for (uint32_t bc = 0; bc < f->block_cols; ++bc) {
+        const uint64_t cell = (uint64_t)br * f->block_cols + bc;
+        for (uint32_t k = bp[cell]; k < bp[cell + 1]; ++k) {
+          rows[k] = (br << lb) + (pk[k] >> 16);
+          cols[k] = (bc << lb) + (pk[k] & 0xFFFFu);
+        }
+      }
+  } else if (f->alg == ORC_MERGEB || f->alg == ORC_MERGEBH) {
+    const uint32_t* brp = ARR(f, "blk_row_ptr", uint32_t);
+    const uint32_t* bci = ARR(f, "blk_col_ind", uint32_t);
+    const uint32_t* bdp = ARR(f, "blk_data_ptr", uint32_t);
+    const uint32_t* pk = ARR(f, "packed", uint32_t);
+    for (uint32_t br = 0; br < f->block_rows; ++br)
+      for (uint32_t t = brp[br]; t < brp[br + 1]; ++t)
+        for (uint32_t k = bdp[t]; k < bdp[t + 1]; ++k) {
+          rows[k] = (br << lb) + (pk[k] >> 16);
+          cols[k] = (bci[t] << lb) + (pk[k] & 0xFFFFu);
+        }
+  } else {
+    return bcoh_replay(f, NULL, NULL, f->bands, rows, cols);
   }
   return ORC_OK;
 }

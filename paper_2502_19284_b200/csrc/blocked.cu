@@ -23,6 +23,60 @@ extern thread_local std::string g_last_error;
 
 namespace {
 
+// Warp-wide in-block coordinate decoder of one chunk, 32 elements per step: packed (row << 16 |
+// col) or ICRS, whose running state (column sum S, row count R, in-block row IR, next row jump
+// rjn) starts from the chunk's precomputed state.
+template <bool ICRS>
+struct ChunkCoords {
+  uint32_t S = 0, IR = 0, rjn = 0;
+  int R = -1;
+
+  __device__ __forceinline__ void start(const uint4* __restrict__ ch_state, uint64_t c) {
+    if (ICRS) {
+      const uint4 st = ch_state[c];
+      S = st.x;
+      R = (int)st.y;
+      IR = st.z;
+      rjn = st.w;
+    }
+  }
+
+  __device__ __forceinline__ void step(const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc,
+                                       const uint16_t* __restrict__ row_jump, uint32_t k, bool valid,
+                                       unsigned lane, unsigned lb, uint64_t pf, uint32_t& ir, uint32_t& ic) {
+    if (!ICRS) {
+      const uint32_t pk = valid ? ld_stream(packed + k, pf) : 0u;
+      ir = pk >> 16;
+      ic = pk & 0xFFFFu;
+    } else {
+      uint32_t inc = valid ? (uint32_t)__ldg(col_inc + k) : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+        if ((int)lane >= off) inc += t;
+      }
+      const uint32_t Sk = S + inc;
+      const int r = (int)(Sk >> lb);
+      ic = Sk & ((1u << lb) - 1u);
+      const int r_last = __shfl_sync(0xFFFFFFFFu, r, 31);
+      const int nnew = r_last - R;
+      uint32_t jv = (int)lane < nnew ? (uint32_t)__ldg(row_jump + rjn + lane) : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, jv, off);
+        if ((int)lane >= off) jv += t;
+      }
+      const int idx = r - R - 1;
+      const uint32_t cum = __shfl_sync(0xFFFFFFFFu, jv, idx > 0 ? idx : 0);
+      ir = idx >= 0 ? IR + cum : IR;
+      S = __shfl_sync(0xFFFFFFFFu, Sk, 31);
+      IR = __shfl_sync(0xFFFFFFFFu, ir, 31);
+      R = r_last;
+      rjn += (uint32_t)nnew;
+    }
+  }
+};
+
 template <bool ICRS>
 __global__ void __launch_bounds__(256) blocked_spmv_kernel(
     const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc,
@@ -33,56 +87,19 @@ __global__ void __launch_bounds__(256) blocked_spmv_kernel(
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t mask = (1u << lb) - 1u;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   for (uint64_t c = gw; c < nchunks; c += nw) {
     const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
     const uint2 rc = blk_rc[ch_blk[c]];
     const uint32_t rbase = rc.x << lb, cbase = rc.y << lb;
-    uint32_t S = 0, IR = 0, rjn = 0;
-    int R = -1;
-    if (ICRS) {
-      const uint4 st = ch_state[c];
-      S = st.x;
-      R = (int)st.y;
-      IR = st.z;
-      rjn = st.w;
-    }
+    ChunkCoords<ICRS> cur;
+    cur.start(ch_state, c);
     for (uint32_t base = e0; base < e1; base += 32) {
       const uint32_t k = base + lane;
       const bool valid = k < e1;
       uint32_t ir, ic;
-      if (!ICRS) {
-        const uint32_t pk = valid ? ld_stream(packed + k, pf) : 0u;
-        ir = pk >> 16;
-        ic = pk & 0xFFFFu;
-      } else {
-        uint32_t inc = valid ? (uint32_t)__ldg(col_inc + k) : 0u;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-          if ((int)lane >= off) inc += t;
-        }
-        const uint32_t Sk = S + inc;
-        const int r = (int)(Sk >> lb);
-        ic = Sk & mask;
-        const int r_last = __shfl_sync(0xFFFFFFFFu, r, 31);
-        const int nnew = r_last - R;
-        uint32_t jv = (int)lane < nnew ? (uint32_t)__ldg(row_jump + rjn + lane) : 0u;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, jv, off);
-          if ((int)lane >= off) jv += t;
-        }
-        const int idx = r - R - 1;
-        const uint32_t cum = __shfl_sync(0xFFFFFFFFu, jv, idx > 0 ? idx : 0);
-        ir = idx >= 0 ? IR + cum : IR;
-        S = __shfl_sync(0xFFFFFFFFu, Sk, 31);
-        IR = __shfl_sync(0xFFFFFFFFu, ir, 31);
-        R = r_last;
-        rjn += (uint32_t)nnew;
-      }
+      cur.step(packed, col_inc, row_jump, k, valid, lane, lb, pf, ir, ic);
       double v = valid ? ld_stream(data + k, pf) * ld_x(x + cbase + ic, pl) : 0.0;
       const uint32_t row = valid ? rbase + ir : 0xFFFFFFFFu;
       // warp segmented sum over runs of equal rows
@@ -176,7 +193,73 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
   }
 }
 
+// csb_/mergeb_/bcoh_to_triplet (csb.hpp:103-120, mergeb.hpp:110-127, bcoh.hpp:379-392): the
+// multiply's chunk walk with the coordinates stored instead of multiplied, at storage positions.
+template <bool ICRS>
+__global__ void __launch_bounds__(256) blocked_decode_kernel(
+    const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc,
+    const uint16_t* __restrict__ row_jump, const uint32_t* __restrict__ ch_begin,
+    const uint32_t* __restrict__ ch_blk, const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc,
+    uint32_t nchunks, unsigned lb, uint32_t* __restrict__ rows, uint32_t* __restrict__ cols) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pf = policy_evict_first();
+  for (uint64_t c = gw; c < nchunks; c += nw) {
+    const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
+    const uint2 rc = blk_rc[ch_blk[c]];
+    ChunkCoords<ICRS> cur;
+    cur.start(ch_state, c);
+    for (uint32_t base = e0; base < e1; base += 32) {
+      const uint32_t k = base + lane;
+      const bool valid = k < e1;
+      uint32_t ir, ic;
+      cur.step(packed, col_inc, row_jump, k, valid, lane, lb, pf, ir, ic);
+      if (valid) {
+        rows[k] = (rc.x << lb) + ir;
+        cols[k] = (rc.y << lb) + ic;
+      }
+    }
+  }
+}
+
+// crs_to_triplet (crs.hpp:94-105): one warp per row writes the row index over its range.
+__global__ void __launch_bounds__(256) crs_rows_kernel(const uint32_t* __restrict__ row_ptr, uint32_t m,
+                                                       uint32_t* __restrict__ rows) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < m; i += nw)
+    for (uint32_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) rows[k] = (uint32_t)i;
+}
+
 }  // namespace
+
+int format_to_triplet(const Format& f, uint32_t* rows, uint32_t* cols, double* vals, cudaStream_t s) {
+  if (f.nnz == 0) return 0;
+  if (vals) cudaMemcpyAsync(vals, f.find("data")->ptr, 8 * f.nnz, cudaMemcpyDeviceToDevice, s);
+  if (f.alg <= 2) {
+    cudaMemcpyAsync(cols, f.find("col_ind")->ptr, 4 * f.nnz, cudaMemcpyDeviceToDevice, s);
+    crs_rows_kernel<<<grid_for((uint64_t)f.m * 32, 256), 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, rows);
+    note_launch();
+    return check_launch("format_to_triplet(crs)");
+  }
+  const DevArray* cb = f.find("chunk_begin");
+  const uint32_t nchunks = (uint32_t)(cb->count() - 1);
+  const unsigned blocks = grid_for((uint64_t)nchunks * 32, 256);
+  const DevArray* pk = f.find("packed");
+  note_launch();
+  if (f.alg == kBcoh)  // ICRS in-block stream; every BCOH variant lists both col_inc and packed
+    blocked_decode_kernel<true><<<blocks, 256, 0, s>>>(
+        nullptr, f.find("col_inc")->as<uint16_t>(), f.find("row_jump")->as<uint16_t>(), cb->as<uint32_t>(),
+        f.find("chunk_blk")->as<uint32_t>(), f.find("chunk_state")->as<uint4>(), f.find("blk_rc")->as<uint2>(),
+        nchunks, f.log2_beta, rows, cols);
+  else
+    blocked_decode_kernel<false><<<blocks, 256, 0, s>>>(
+        pk->as<uint32_t>(), nullptr, nullptr, cb->as<uint32_t>(), f.find("chunk_blk")->as<uint32_t>(), nullptr,
+        f.find("blk_rc")->as<uint2>(), nchunks, f.log2_beta, rows, cols);
+  return check_launch("format_to_triplet(blocked)");
+}
 
 int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.m) cudaMemsetAsync(y, 0, sizeof(double) * f.m, s);

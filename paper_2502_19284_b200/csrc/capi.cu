@@ -570,6 +570,13 @@ int spmvlab_cuda_bicrs_to_triplet(const spmvlab_cuda_bicrs* a, uint32_t* rows, u
   return bicrs_decode_all(*a, rows, cols, nullptr, static_cast<cudaStream_t>(stream));
 }
 
+int spmvlab_cuda_format_to_triplet(const spmvlab_cuda_format* f, uint32_t* rows, uint32_t* cols, double* vals,
+                                   void* stream) {
+  if (!f || (f->nnz && (!rows || !cols))) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  return format_to_triplet(*f, rows, cols, vals, static_cast<cudaStream_t>(stream));
+}
+
 int spmvlab_cuda_csb_work_items(const spmvlab_cuda_format* f, uint64_t split_threshold,
                                 spmvlab_cuda_csb_item* items, uint64_t capacity, uint64_t* count,
                                 void* stream) {

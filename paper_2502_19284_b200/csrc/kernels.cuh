@@ -85,6 +85,7 @@ int crs_to_icrs(const Format& f, spmvlab_cuda_bicrs* out, cudaStream_t s);
 int triplet_to_bicrs(const spmvlab_cuda_coo& a, const uint32_t* order, spmvlab_cuda_bicrs* out, cudaStream_t s);
 int bicrs_decode_all(const spmvlab_cuda_bicrs& b, uint32_t* rows, uint32_t* cols, uint64_t* stats, cudaStream_t s);
 int bicrs_spmv(const spmvlab_cuda_bicrs& b, const double* x, double* y, uint64_t* stats, cudaStream_t s);
+int format_to_triplet(const Format& f, uint32_t* rows, uint32_t* cols, double* vals, cudaStream_t s);
 int csb_work_items(const Format& f, uint64_t split_threshold, spmvlab_cuda_csb_item* items, uint64_t capacity,
                    uint64_t* count, cudaStream_t s);
 

@@ -466,6 +466,35 @@ def crs_to_icrs(fmt: BuiltFormat, stream=None) -> IncrementalRowStorage:
     return IncrementalRowStorage(c)
 
 
+def format_to_triplet(fmt: BuiltFormat, stream=None) -> TripletMatrix:
+    """crs_/csb_/mergeb_/bcoh_to_triplet (crs.hpp:94-105, csb.hpp:103-120, mergeb.hpp:110-127,
+    bcoh.hpp:379-392): the elements of any built format in the reference's output order (storage
+    order, BCOH band by band), decoded on the device."""
+    nnz = fmt.nnz()
+    r = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    c = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    v = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    ptr = (lambda t: t.data_ptr() if nnz else None)
+    _check(capi.load().spmvlab_cuda_format_to_triplet(fmt.handle, ptr(r), ptr(c), ptr(v), _stream(stream)))
+    return TripletMatrix(fmt.m, fmt.n, r, c, v)
+
+
+def _family_to_triplet(algs, what):
+    def fn(fmt: BuiltFormat, stream=None) -> TripletMatrix:
+        if int(fmt.alg) not in algs:
+            raise Error(ErrorKind.InvalidArgument, f"{what} needs a {what.split('_')[0].upper()} format")
+        return format_to_triplet(fmt, stream)
+    fn.__name__ = what
+    fn.__doc__ = f"{what}: format_to_triplet restricted to its format family."
+    return fn
+
+
+crs_to_triplet = _family_to_triplet((0, 1, 2), "crs_to_triplet")
+csb_to_triplet = _family_to_triplet((3, 4), "csb_to_triplet")
+bcoh_to_triplet = _family_to_triplet((5, 6, 7, 8), "bcoh_to_triplet")
+mergeb_to_triplet = _family_to_triplet((9, 10), "mergeb_to_triplet")
+
+
 CSB_ITEM_DTYPE = np.dtype([("block_row", np.uint32), ("cell_begin", np.uint32), ("cell_end", np.uint32),
                            ("temp_slot", np.int32), ("elem_begin", np.uint64), ("elem_end", np.uint64)])
 
