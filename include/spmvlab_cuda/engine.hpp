@@ -256,6 +256,43 @@ Vec run_spmv(Algorithm alg, const BuiltFormat& f, const Vec& x, unsigned p, cons
   return y;
 }
 
+// crs_to_triplet / csb_to_triplet / mergeb_to_triplet / bcoh_to_triplet (crs.hpp:94, csb.hpp:103,
+// mergeb.hpp:110, bcoh.hpp:379) for any format: a host triplet (any type with the TripletMatrix
+// members) in the reference's output order.
+template <typename Triplet>
+Triplet to_triplet(const BuiltFormat& f) {
+  const std::size_t nnz = f.nnz();
+  DeviceBuffer r(4 * nnz), c(4 * nnz), v(8 * nnz);
+  check(spmvlab_cuda_format_to_triplet(f.handle(), r.as<std::uint32_t>(), c.as<std::uint32_t>(), v.as<double>(),
+                                       nullptr));
+  Triplet t;
+  t.m = f.m();
+  t.n = f.n();
+  t.row_ind.resize(nnz);
+  t.col_ind.resize(nnz);
+  t.data.resize(nnz);
+  if (nnz) {
+    check_cuda(cudaMemcpy(t.row_ind.data(), r.as<void>(), 4 * nnz, cudaMemcpyDeviceToHost));
+    check_cuda(cudaMemcpy(t.col_ind.data(), c.as<void>(), 4 * nnz, cudaMemcpyDeviceToHost));
+    check_cuda(cudaMemcpy(t.data.data(), v.as<void>(), 8 * nnz, cudaMemcpyDeviceToHost));
+  }
+  return t;
+}
+
+// The CsbWorkItem list spmv_csb builds (spmv_parallel.hpp:202-264), host copy.
+inline std::vector<spmvlab_cuda_csb_item> csb_work_items(const BuiltFormat& f, std::size_t split_threshold = 0) {
+  std::uint64_t count = 0;
+  check(spmvlab_cuda_csb_work_items(f.handle(), split_threshold, nullptr, 0, &count, nullptr));
+  std::vector<spmvlab_cuda_csb_item> out(count);
+  if (count) {
+    DeviceBuffer d(sizeof(spmvlab_cuda_csb_item) * count);
+    check(spmvlab_cuda_csb_work_items(f.handle(), split_threshold, d.as<spmvlab_cuda_csb_item>(), count, &count,
+                                      nullptr));
+    check_cuda(cudaMemcpy(out.data(), d.as<void>(), sizeof(spmvlab_cuda_csb_item) * count, cudaMemcpyDeviceToHost));
+  }
+  return out;
+}
+
 inline StorageBreakdown storage_report(const BuiltFormat& f) {
   spmvlab_cuda_storage_array rows[16];
   std::size_t count = 0;

@@ -79,6 +79,27 @@ static void check_matrix(const TripletMatrix& a, const std::string& tag, std::ui
         EXPECT(got.size() == ra.bytes && (ra.bytes == 0 || std::memcmp(got.data(), ra.data, ra.bytes) == 0),
                "%s %s array %s differs", tag.c_str(), sc::algorithm_name(alg), ra.name);
       }
+      {  // *_to_triplet: storage-order coordinates and values bitwise the oracle's
+        const TripletMatrix t = sc::to_triplet<TripletMatrix>(f);
+        const std::size_t nnz = a.data.size();
+        std::vector<std::uint32_t> rr(nnz), rc(nnz);
+        std::vector<double> rv(nnz);
+        orc_format_to_triplet(ref, rr.data(), rc.data(), rv.data());
+        EXPECT(t.row_ind == rr && t.col_ind == rc && t.data == rv, "%s %s to_triplet differs", tag.c_str(),
+               sc::algorithm_name(alg));
+      }
+      if (alg == sc::Algorithm::Csb || alg == sc::Algorithm::Csbh) {
+        for (std::size_t thr : {std::size_t{0}, std::size_t{1}, std::size_t{9}}) {
+          const std::vector<spmvlab_cuda_csb_item> got = sc::csb_work_items(f, thr);
+          std::uint64_t cnt = 0;
+          orc_csb_work_items(ref, thr, nullptr, 0, &cnt);
+          std::vector<orc_csb_item> want(cnt);
+          orc_csb_work_items(ref, thr, want.data(), cnt, &cnt);
+          EXPECT(got.size() == want.size() &&
+                     (want.empty() || std::memcmp(got.data(), want.data(), sizeof(orc_csb_item) * cnt) == 0),
+                 "%s %s csb_work_items(%zu) differs", tag.c_str(), sc::algorithm_name(alg), thr);
+        }
+      }
       const std::vector<double> y = sc::run_spmv(alg, f, x, p, opt);
       std::vector<double> yr(a.m);
       orc_run_spmv(static_cast<int>(alg), ref, x.data(), x.size(), yr.data(), yr.size(), p, 0);
