@@ -594,6 +594,8 @@ static int blocked_common(BlockedBuild& bb, const spmvlab_cuda_coo& a, const uin
 // sector per element; the window kernel turns that into shared-memory adds (R-MAT s22: 831 ->
 // 637 us).  Row-major MergeB blocks give coalesced runs and stay on the reduction kernel, which
 // is faster there (335 vs 465 us).  SPMVLAB_BLOCKED_WINDOW=0 disables, =1 forces for all four.
+// Chunks per window item: R-MAT s22 CSB 741 / 671 / 636 / 667 / 711 / 1226 us at 64 / 128 / 256 /
+// 512 / 1024 / 4096 (window zero + write-out per item vs. the tail of one 1024-thread CTA per SM).
 constexpr uint32_t kWinChunks = 256;
 
 // `permute`: the block rows are not contiguous in storage (BCOH's Hilbert-ordered blocks), so the
