@@ -260,10 +260,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SPMVLAB_BENCH_BACKEND=gloo (test only): N ranks as processes sharing fewer GPUs, synchronised
+    # on the host (no kernel waits on another rank), to exercise the N > 1 flow on a 1-GPU box.
+    backend = os.environ.get("SPMVLAB_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         if world > 1:
