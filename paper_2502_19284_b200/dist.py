@@ -114,7 +114,13 @@ class FusedExchangeSpMV:
         self.lo, self.hi = self.cuts[rank], self.cuts[rank + 1]
         self.fmt, self.n = fmt, n
         self.device = torch.device("cuda", torch.cuda.current_device())
+        self.group = group
         self.barrier = barrier or (lambda: dist.barrier(group))
+        # Over NCCL the end-of-step rendezvous is a stream-ordered 1-element all-reduce: a rank's
+        # next multiply cannot start before every rank's scatter kernels completed (their peer
+        # stores are performed at kernel completion), and the host never waits.
+        self._stream_barrier = barrier is None and dist.get_backend(group) == "nccl"
+        self._token = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.own, handles, err = [], [], None
         try:
             for _ in range(2):
@@ -176,8 +182,13 @@ class FusedExchangeSpMV:
         self._check(self.capi.load().spmvlab_cuda_run_spmv_scatter(
             self.fmt.handle, self.ptr[self.cur][self.rank], self.n, y_local, self.hi - self.lo, dest, len(peers),
             self.lo, st.cuda_stream))
-        st.synchronize()
-        self.barrier()  # every rank's rows have landed in every next buffer
+        if self._stream_barrier:
+            import torch.distributed as dist
+            with torch.cuda.stream(st):
+                dist.all_reduce(self._token, group=self.group)
+        else:
+            st.synchronize()
+            self.barrier()  # every rank's rows have landed in every next buffer
         self.cur = nxt
 
     def iterate(self, x0: torch.Tensor, iters: int) -> torch.Tensor:
