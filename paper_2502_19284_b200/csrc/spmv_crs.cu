@@ -16,7 +16,10 @@
 //        col_ind / data entries with one 128-bit and one 256-bit load, gathers and multiplies in
 //        registers (two passes in flight); row ends of the pass are scattered to the element they
 //        close through a 128-entry shared map, each lane walks its 4 products, one warp segmented
-//        scan joins the lanes.  No product staging.  cfg2: 297 us.
+//        scan joins the lanes.  No product staging.  cfg2: 291 us (+ fix-up).  Folding the fix-up
+//        into the kernel measured slower: a look-back spin on the previous tile's carry 407 us, a
+//        last-arrival counter per spanning row (fence + atomic at each tile end) 356 us -- the
+//        tile-end latency holds warp slots this latency-bound kernel needs.
 //      - kVariantWarpStage (256 x 7): one tile of 32*IPT items per WARP in warp-private
 //        shared memory, warp synchronisation only: coalesced streaming loads of row ends /
 //        col_ind / data (all IPT in flight per lane), IPT x gathers in flight, products staged,
