@@ -119,6 +119,23 @@ def ncu_traffic(cfg: int, kernel: str):
     return e.get("dram_bytes_per_launch") if e else None
 
 
+def l2_roofline(cfg: int, kernel: str, kernel_ms: float):
+    """The roofline that binds the gather kernels: whole 32-byte L2 sectors per random 8-byte x
+    gather, L2 -> SM bytes (ncu, per launch) over the kernel time, against the same rate of the
+    pure x-gather probe (tools/microbench.py gather_x; no merge logic)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e, probe = d.get(f"cfg{cfg}:{kernel}"), d.get("probe:gather_x")
+    if not e or "l2_to_sm_bytes_per_launch" not in e or not probe:
+        return None
+    achieved = e["l2_to_sm_bytes_per_launch"] / (kernel_ms / 1e3) / 1e9
+    peak = probe["l2_to_sm_bytes_per_launch"] / (probe["us"] / 1e6) / 1e9
+    return {"bytes_per_launch": e["l2_to_sm_bytes_per_launch"], "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "peak_kind": "probe (x-gather only kernel)"}
+
+
 def ev_time(fn, reps: int, warmup: int, stream) -> list:
     for _ in range(warmup):
         fn()
@@ -384,7 +401,7 @@ def main():
     roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg_bytes, "traffic": ncu_traffic(args.config, kernel_name),
-                "share_of_step": k_ms / ms_step}
+                "share_of_step": k_ms / ms_step, "l2_sectors": l2_roofline(args.config, kernel_name, k_ms)}
 
     # End to end through the C ABI with host buffers: every step copies its own x in (pinned H2D),
     # multiplies, and copies its own y out (D2H).  Steps rotate over three streams with their own

@@ -18,7 +18,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "sm__cycles_elapsed.avg.per_second",
-        "launch__grid_size", "launch__block_size"]
+        "launch__grid_size", "launch__block_size", "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_requests.sum"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -53,6 +53,8 @@ def full(rep, out, kernel, config, summary):
     js[f"cfg{config}:{kernel}"] = {"dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
                                    "dram_read": num("dram__bytes_read.sum"), "dram_write": num("dram__bytes_write.sum"),
                                    "source": os.path.relpath(out, ROOT)}
+    if "l1tex__m_xbar2l1tex_read_bytes.sum" in d:  # L2 -> SM bytes (gathers move whole 32 B sectors)
+        js[f"cfg{config}:{kernel}"]["l2_to_sm_bytes_per_launch"] = num("l1tex__m_xbar2l1tex_read_bytes.sum")
     json.dump(js, open(summary, "w"), indent=1)
     print("\n".join(lines))
 
