@@ -11,7 +11,11 @@
 // ICRS decoded with two warp prefix sums (in_col = S mod beta, row changes = S / beta, the row
 // jumps of the new rows summed with a second scan), a warp segmented reduction over runs of equal
 // rows, and one fp64 reduction into y per run (y is cleared first, as the reference engines clear
-// their output rows, spmv_parallel.hpp:277-281 and :344-345).
+// their output rows, spmv_parallel.hpp:277-281 and :344-345).  (A lane-blocked form -- 4
+// consecutive elements per lane, 128-bit index / 256-bit data loads, one ICRS scan and one
+// segmented scan per 128 elements -- measured slower on R-MAT s22: BCOH 532 vs 462, BCOHC 411 vs
+// 337, MergeB 423 vs 334 us: rows end almost every element there, and the per-lane fp64
+// reductions of lane-strided rows coalesce worse than the 32 consecutive rows of a warp step.)
 #include <string>
 
 #include "common.cuh"
