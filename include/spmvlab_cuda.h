@@ -73,6 +73,14 @@ int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threa
                               const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
                               void* stream);
 
+/* The per-format builders with an explicit block size beta = 2^log2_beta:
+ * build_csb(a, beta, ZMorton|Hilbert) (inc/csb.hpp:51-57) for algorithms 3/4,
+ * build_mergeb(a, beta, hilbert_inside) (inc/mergeb.hpp:50-56) for 9/10,
+ * build_bcoh(a, beta, p = threads, variant) (inc/bcoh.hpp:194-205) for 5-8.
+ * InvalidArgument: a CRS algorithm, beta outside [2, 2^16] ([2, 2^15] for BCOH), p < 1. */
+int spmvlab_cuda_build_format_beta(int alg, const spmvlab_cuda_coo* a, unsigned log2_beta, unsigned threads,
+                                   spmvlab_cuda_format** out, void* stream);
+
 /* run_spmv(Algorithm, const BuiltFormat&, const DenseVector& x, DenseVector& y, p, opt)
  * -- inc/engine.hpp:126-148.  y (length m) is fully overwritten.  p must be >= 1 and, for BCOH,
  * equal to the band count (inc/spmv_parallel.hpp:339-341). */

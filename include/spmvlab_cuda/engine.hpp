@@ -203,9 +203,9 @@ class BuiltFormat {
   mutable DeviceBuffer x_stage_, y_stage_;
 };
 
-// build_format (inc/engine.hpp:96-122) from a host triplet.
-template <typename Triplet>
-BuiltFormat build_format(Algorithm alg, const Triplet& a, unsigned threads, const EngineOptions& opt = {}) {
+// Uploads a host triplet and runs `build` on the device COO view.
+template <typename Triplet, typename Build>
+BuiltFormat build_from_host(Algorithm alg, const Triplet& a, Build&& build) {
   const std::size_t nnz = a.data.size();
   if (a.row_ind.size() != nnz || a.col_ind.size() != nnz)
     throw Error(ErrorKind::InvalidArgument, "triplet arrays must have equal length");
@@ -217,10 +217,27 @@ BuiltFormat build_format(Algorithm alg, const Triplet& a, unsigned threads, cons
   }
   const spmvlab_cuda_coo coo{static_cast<std::uint32_t>(a.m), static_cast<std::uint32_t>(a.n), nnz,
                              r.as<std::uint32_t>(), c.as<std::uint32_t>(), v.as<double>()};
-  const spmvlab_cuda_options o = opt.c();
   spmvlab_cuda_format* f = nullptr;
-  check(spmvlab_cuda_build_format(static_cast<int>(alg), &coo, threads, &o, &f, nullptr));
+  check(build(&coo, &f));
   return BuiltFormat(alg, f);
+}
+
+// build_format (inc/engine.hpp:96-122) from a host triplet.
+template <typename Triplet>
+BuiltFormat build_format(Algorithm alg, const Triplet& a, unsigned threads, const EngineOptions& opt = {}) {
+  const spmvlab_cuda_options o = opt.c();
+  return build_from_host(alg, a, [&](const spmvlab_cuda_coo* coo, spmvlab_cuda_format** f) {
+    return spmvlab_cuda_build_format(static_cast<int>(alg), coo, threads, &o, f, nullptr);
+  });
+}
+
+// build_csb / build_mergeb / build_bcoh with an explicit block size 2^log2_beta (inc/csb.hpp:51,
+// inc/mergeb.hpp:50, inc/bcoh.hpp:194; `threads` = the BCOH band count p).
+template <typename Triplet>
+BuiltFormat build_format_beta(Algorithm alg, const Triplet& a, unsigned log2_beta, unsigned threads = 1) {
+  return build_from_host(alg, a, [&](const spmvlab_cuda_coo* coo, spmvlab_cuda_format** f) {
+    return spmvlab_cuda_build_format_beta(static_cast<int>(alg), coo, log2_beta, threads, f, nullptr);
+  });
 }
 
 // Stream-ordered multiply on device pointers (no synchronisation).

@@ -139,6 +139,9 @@ class Oracle:
         L.orc_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.orc_free.argtypes = [C.c_void_p]
+        L.orc_build_format_beta.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                            C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.c_uint, C.c_uint,
+                                            C.POINTER(C.POINTER(OrcFormat))]
         L.orc_format_to_triplet.argtypes = [C.POINTER(OrcFormat), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                             C.POINTER(C.c_double)]
         L.orc_csb_work_items.argtypes = [C.POINTER(OrcFormat), C.c_uint64, C.c_void_p, C.c_uint64,
@@ -153,6 +156,20 @@ class Oracle:
                                        _p(vals, C.c_double), threads, l2_bytes, C.byref(fp))
         if rc:
             raise CheckerError(rc, "orc_build_format")
+        try:
+            meta, arrays, storage = _export(fp)
+        finally:
+            self.lib.orc_free_format(fp)
+        return Built(meta, arrays, storage, handle=None)
+
+    def build_beta(self, alg: int, m: int, n: int, rows, cols, vals, log2_beta: int, threads: int = 1) -> Built:
+        """build_csb / build_mergeb / build_bcoh with an explicit block size."""
+        rows, cols, vals = _coo_args(rows, cols, vals)
+        fp = C.POINTER(OrcFormat)()
+        rc = self.lib.orc_build_format_beta(alg, m, n, len(vals), _p(rows, C.c_uint32), _p(cols, C.c_uint32),
+                                            _p(vals, C.c_double), log2_beta, threads, C.byref(fp))
+        if rc:
+            raise CheckerError(rc, "orc_build_format_beta")
         try:
             meta, arrays, storage = _export(fp)
         finally:
@@ -359,6 +376,9 @@ class Reference:
         L.ref_cache_write.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
         L.ref_free_buf.argtypes = [C.c_void_p]
+        L.ref_build_beta.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.c_uint, C.c_uint,
+                                     C.POINTER(C.c_void_p)]
         L.ref_to_triplet.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_double)]
         L.ref_csb_leaves.restype = C.c_int64
@@ -393,6 +413,22 @@ class Reference:
                 built.meta, built.arrays, built.storage = _export(fp)
             finally:
                 self.lib.ref_free_export(fp)
+        return built
+
+    def build_beta(self, alg: int, m: int, n: int, rows, cols, vals, log2_beta: int, threads: int = 1) -> Built:
+        rows, cols, vals = _coo_args(rows, cols, vals)
+        h = C.c_void_p()
+        rc = self.lib.ref_build_beta(alg, m, n, len(vals), _p(rows, C.c_uint32), _p(cols, C.c_uint32),
+                                     _p(vals, C.c_double), log2_beta, threads, C.byref(h))
+        if rc:
+            self._err(rc, "ref_build_beta")
+        built = Built({"alg": alg, "m": m, "n": n, "nnz": len(vals)}, handle=_RefHandle(self.lib, h))
+        fp = C.POINTER(OrcFormat)()
+        self.lib.ref_export(h, C.byref(fp))
+        try:
+            built.meta, built.arrays, built.storage = _export(fp)
+        finally:
+            self.lib.ref_free_export(fp)
         return built
 
     def spmv(self, built: Built, alg: int, x, p: int = 1, split_threshold: int = 0):

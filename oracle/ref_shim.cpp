@@ -80,6 +80,37 @@ int ref_build(int alg, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* row
   }
 }
 
+// The reference's per-format builders with an explicit block size (csb.hpp:51, mergeb.hpp:50,
+// bcoh.hpp:194); threads = band count p for BCOH.
+int ref_build_beta(int alg, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows, const uint32_t* cols,
+                   const double* vals, unsigned log2_beta, unsigned threads, void** out) {
+  try {
+    auto a = make_triplet(m, n, nnz, rows, cols, vals);
+    const BlockSize bs = make_block_size(log2_beta);
+    const auto A = static_cast<Algorithm>(alg);
+    BuiltFormat f;
+    switch (A) {
+      case Algorithm::Csb: f = build_csb(a, bs, CurveKind::ZMorton, 1); break;
+      case Algorithm::Csbh: f = build_csb(a, bs, CurveKind::Hilbert, 1); break;
+      case Algorithm::MergeB: f = build_mergeb(a, bs, false, 1); break;
+      case Algorithm::MergeBH: f = build_mergeb(a, bs, true, 1); break;
+      case Algorithm::Bcoh: f = build_bcoh(a, bs, threads, bcoh_variant, 1); break;
+      case Algorithm::Bcohc: f = build_bcoh(a, bs, threads, bcohc_variant, 1); break;
+      case Algorithm::Bcohch: f = build_bcoh(a, bs, threads, bcohch_variant, 1); break;
+      case Algorithm::Bcohchp: f = build_bcoh(a, bs, threads, bcohchp_variant, 1); break;
+      default: g_err = "no block size for CRS"; return 2;
+    }
+    *out = new Handle{A, std::move(f)};
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
 void ref_free(void* h) { delete static_cast<Handle*>(h); }
 
 int ref_run(void* hv, int alg, const double* x, uint64_t x_len, double* y, uint64_t y_len,

@@ -758,6 +758,27 @@ int orc_build_format(int alg, uint32_t m, uint32_t n, uint64_t nnz, const uint32
   }
 }
 
+/* build_csb / build_mergeb / build_bcoh with an explicit block size (csb.hpp:51-57,
+ * mergeb.hpp:50-56, bcoh.hpp:194-205): beta in [2, 2^16] ([2, 2^15] for BCOH), p >= 1. */
+int orc_build_format_beta(int alg, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows,
+                          const uint32_t* cols, const double* vals, unsigned log2_beta, unsigned threads,
+                          orc_format** out) {
+  *out = NULL;
+  if (alg <= ORC_MERGE || alg > ORC_MERGEBH) return ORC_INVALID_ARGUMENT;
+  if (nnz > UINT32_MAX) return ORC_OVERFLOW;
+  const unsigned cap = is_bcoh(alg) ? 15u : 16u;
+  if (log2_beta < 1 || log2_beta > cap) return ORC_INVALID_ARGUMENT;
+  switch (alg) {
+    case ORC_CSB: case ORC_CSBH:
+      return build_csb(alg, m, n, (uint32_t)nnz, rows, cols, vals, log2_beta, out);
+    case ORC_MERGEB: case ORC_MERGEBH:
+      return build_mergeb(alg, m, n, (uint32_t)nnz, rows, cols, vals, log2_beta, out);
+    default:
+      if (threads < 1) return ORC_INVALID_ARGUMENT;
+      return build_bcoh(alg, m, n, (uint32_t)nnz, rows, cols, vals, log2_beta, threads, out);
+  }
+}
+
 /* ---------------------------------------------------------------- kernels */
 
 /* spmv_crs_seq, crs.hpp:43-57 (ParCRS is bitwise equal, spmv_parallel.hpp:106-125) */

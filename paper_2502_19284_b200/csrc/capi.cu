@@ -208,9 +208,7 @@ int spmvlab_cuda_partition_rows_by_nnz(const uint32_t* prefix, uint32_t m, unsig
   return partition_rows_by_nnz_host(prefix, m, p, lb, bounds);
 }
 
-int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threads,
-                              const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
-                              void* stream) {
+static int check_coo(int alg, const spmvlab_cuda_coo* a, spmvlab_cuda_format** out) {
   if (!out || !a) return fail(kInvalidArgument, "null argument");
   *out = nullptr;
   if (alg < 0 || alg >= kAlgCount) return fail(kInvalidArgument, "unknown algorithm");
@@ -218,8 +216,35 @@ int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threa
     return fail(kOverflow, "matrix dimension exceeds the supported index width");
   if (a->nnz > 0xFFFFFFFFull) return fail(kOverflow, "nnz does not fit the 32-bit index type");
   if (a->nnz && (!a->row_ind || !a->col_ind || !a->data)) return fail(kInvalidArgument, "null COO array");
+  return kOk;
+}
+
+static int build_with_beta(int alg, const spmvlab_cuda_coo* a, unsigned threads, unsigned lb, uint64_t split,
+                           spmvlab_cuda_format** out, void* stream);
+
+int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threads,
+                              const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
+                              void* stream) {
+  if (int rc = check_coo(alg, a, out)) return rc;
   const uint64_t l2 = opt ? opt->l2_bytes : 512 * 1024;
   const uint64_t split = opt ? opt->split_threshold : 0;
+  return build_with_beta(alg, a, threads, engine_log2_beta(alg, a->n, l2), split, out, stream);
+}
+
+int spmvlab_cuda_build_format_beta(int alg, const spmvlab_cuda_coo* a, unsigned log2_beta, unsigned threads,
+                                   spmvlab_cuda_format** out, void* stream) {
+  if (int rc = check_coo(alg, a, out)) return rc;
+  if (is_crs_alg(alg)) return fail(kInvalidArgument, "CRS formats take no block size");
+  const bool bcoh = !is_csb_alg(alg) && !is_mergeb_alg(alg);
+  if (log2_beta < 1 || log2_beta > (bcoh ? 15u : 16u))
+    return fail(kInvalidArgument, bcoh ? "block size outside the 15-bit increment cap"
+                                       : "block size outside the 16-bit packing cap");
+  if (bcoh && threads < 1) return fail(kInvalidArgument, "band count must be >= 1");
+  return build_with_beta(alg, a, threads, log2_beta, 0, out, stream);
+}
+
+static int build_with_beta(int alg, const spmvlab_cuda_coo* a, unsigned threads, unsigned lb, uint64_t split,
+                           spmvlab_cuda_format** out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* f = new (std::nothrow) spmvlab_cuda_format();
   if (!f) return fail(kNoMemory, "host allocation failed");
@@ -227,7 +252,6 @@ int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threa
   f->m = a->m;
   f->n = a->n;
   f->nnz = a->nnz;
-  const unsigned lb = engine_log2_beta(alg, a->n, l2);
   int rc;
   {
     Arena ar(s);

@@ -223,6 +223,16 @@ def build_format(alg, a: TripletMatrix, threads: int = 1, opt: EngineOptions | N
     return BuiltFormat(h.value, alg)
 
 
+def build_format_beta(alg, a: TripletMatrix, log2_beta: int, threads: int = 1, stream=None) -> BuiltFormat:
+    """The per-format builders with an explicit block size 2^log2_beta: build_csb (inc/csb.hpp:51),
+    build_mergeb (inc/mergeb.hpp:50), build_bcoh with p = threads bands (inc/bcoh.hpp:194)."""
+    h = C.c_void_p()
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_build_format_beta(int(alg), C.byref(coo), int(log2_beta), int(threads),
+                                                      C.byref(h), _stream(stream)))
+    return BuiltFormat(h.value, alg)
+
+
 def run_spmv(alg, fmt: BuiltFormat, x: torch.Tensor, y: torch.Tensor | None = None, p: int = 1,
              opt: EngineOptions | None = None, stream=None) -> torch.Tensor:
     """inc/engine.hpp:126-156: y = A x on the device (stream-ordered; y fully overwritten)."""

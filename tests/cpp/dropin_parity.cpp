@@ -123,6 +123,35 @@ int main() {
     const std::vector<double> y = sc::run_spmv(alg, f, std::vector<double>(4, 1.0), 2);
     EXPECT(y == (std::vector<double>{3, 3, 0, 9}), "e4 %s", sc::algorithm_name(alg));
   }
+  // build_format_beta: the per-format builders at explicit block sizes, every array bitwise the oracle's
+  {
+    const TripletMatrix a = random_matrix(200, 150, 0.04, 21, 150);
+    for (sc::Algorithm alg : sc::all_algorithms) {
+      if (static_cast<int>(alg) <= 2) continue;
+      for (unsigned lb : {1u, 3u, 6u}) {
+        const unsigned p = 3;
+        sc::BuiltFormat f = sc::build_format_beta(alg, a, lb, p);
+        orc_format* ref = nullptr;
+        const int rc = orc_build_format_beta(static_cast<int>(alg), a.m, a.n, a.data.size(), a.row_ind.data(),
+                                             a.col_ind.data(), a.data.data(), lb, p, &ref);
+        EXPECT(rc == 0, "oracle build_beta failed");
+        for (int i = 0; rc == 0 && i < ref->nstorage; ++i) {
+          const orc_array& ra = ref->arrays[i];
+          const std::vector<unsigned char> got = f.download<unsigned char>(ra.name);
+          EXPECT(got.size() == ra.bytes && (ra.bytes == 0 || std::memcmp(got.data(), ra.data, ra.bytes) == 0),
+                 "build_format_beta %s lb %u array %s differs", sc::algorithm_name(alg), lb, ra.name);
+        }
+        orc_free_format(ref);
+      }
+    }
+    bool thrown = false;
+    try {
+      sc::build_format_beta(sc::Algorithm::Bcoh, a, 16, 2);
+    } catch (const sc::Error& e) {
+      thrown = e.kind() == sc::ErrorKind::InvalidArgument;
+    }
+    EXPECT(thrown, "BCOH beta 2^16 not rejected");
+  }
   check_matrix(random_matrix(300, 250, 0.03, 11, 250), "rand300", 4096);
   check_matrix(random_matrix(1000, 1200, 0.01, 12), "rand1000", 512 * 1024);
   check_matrix(random_matrix(77, 5, 0.3, 13), "tall", 64);
