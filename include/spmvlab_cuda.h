@@ -148,6 +148,10 @@ void spmvlab_cuda_free_format(spmvlab_cuda_format* f);
 /* validate(const TripletMatrix&) -- inc/triplet.hpp:42-59 (range + duplicate check on device). */
 int spmvlab_cuda_validate(const spmvlab_cuda_coo* a, void* stream);
 
+/* row_counts + row_prefix (inc/triplet.hpp:75-87): prefix (device, m + 1 entries) = exclusive
+ * prefix sums of the entries per row.  IndexOutOfRange for a row >= m.  Synchronises `stream`. */
+int spmvlab_cuda_row_prefix(const spmvlab_cuda_coo* a, uint32_t* prefix, void* stream);
+
 /* --- SPMVLAB1 binary triplet cache (inc/cache_io.hpp:31-91, inc/io.hpp:29-40) ----------------- */
 
 /* cache_read: tag "SPMVLAB1", m, n, nnz as u64 LE, then nnz u64 row indices, nnz u64 column

@@ -5,7 +5,7 @@ host mirror of the reference's algorithm interface (inc/engine.hpp).
 """
 from .engine import (  # noqa: F401
     Algorithm, BuiltFormat, EngineOptions, Error, ErrorKind, StorageBreakdown, TripletMatrix,
-    algorithm_from_name, algorithm_name, all_algorithms, build_format, build_format_beta, cache_read, cache_write, curve_keys,
+    algorithm_from_name, algorithm_name, all_algorithms, build_format, build_format_beta, row_prefix, cache_read, cache_write, curve_keys,
     MatrixHeader, load_matrix, read_matrix_market, read_matrix_market_host,
     IncrementalRowStorage, bicrs_from_arrays, crs_to_icrs, triplet_to_bicrs,
     CSB_ITEM_DTYPE, csb_items_numpy, csb_work_items,

@@ -27,7 +27,7 @@ EXPORTS = [
     "spmvlab_cuda_triplet_to_bicrs", "spmvlab_cuda_bicrs_spmv", "spmvlab_cuda_bicrs_to_triplet",
     "spmvlab_cuda_free_bicrs", "spmvlab_cuda_exchange_alloc", "spmvlab_cuda_exchange_open",
     "spmvlab_cuda_exchange_close", "spmvlab_cuda_run_spmv_scatter", "spmvlab_cuda_csb_work_items",
-    "spmvlab_cuda_format_to_triplet", "spmvlab_cuda_build_format_beta",
+    "spmvlab_cuda_format_to_triplet", "spmvlab_cuda_build_format_beta", "spmvlab_cuda_row_prefix",
 ]
 
 
@@ -98,6 +98,7 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_free_bicrs.restype = None
     L.spmvlab_cuda_csb_work_items.argtypes = [vp, u64, vp, u64, C.POINTER(u64), vp]
     L.spmvlab_cuda_format_to_triplet.argtypes = [vp, vp, vp, vp, vp]
+    L.spmvlab_cuda_row_prefix.argtypes = [C.POINTER(Coo), vp, vp]
     L.spmvlab_cuda_build_format_beta.argtypes = [i, C.POINTER(Coo), C.c_uint, C.c_uint, C.POINTER(vp), vp]
     L.spmvlab_cuda_exchange_alloc.argtypes = [u64, C.POINTER(vp), C.POINTER(C.c_ubyte)]
     L.spmvlab_cuda_exchange_open.argtypes = [C.POINTER(C.c_ubyte), C.POINTER(vp)]

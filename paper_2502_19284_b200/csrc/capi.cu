@@ -477,6 +477,15 @@ int spmvlab_cuda_validate(const spmvlab_cuda_coo* a, void* stream) {
   return rc;
 }
 
+int spmvlab_cuda_row_prefix(const spmvlab_cuda_coo* a, uint32_t* prefix, void* stream) {
+  if (!a || !prefix || (a->nnz && !a->row_ind)) return fail(kInvalidArgument, "null argument");
+  g_last_error.clear();
+  Arena ar(static_cast<cudaStream_t>(stream));
+  const int rc = row_prefix(*a, prefix, ar);
+  if (rc == kIndexOutOfRange) return fail(rc, "index out of range: row outside the matrix shape");
+  return rc;
+}
+
 int spmvlab_cuda_merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b,
                                    uint64_t b_len, const uint64_t* diags, uint64_t count,
                                    uint64_t* out_i, void* stream) {

@@ -32,7 +32,43 @@ __global__ void curve_keys_kernel(int kind, const uint32_t* __restrict__ rows,
     keys[k] = kind == 0 ? morton_encode(rows[k], cols[k], level) : hilbert_encode_t(rows[k], cols[k], level, s_henc);
 }
 
+// row_counts (inc/triplet.hpp:75-80): warp-aggregated increments (entries of one row that meet in
+// a warp add once); rows out of range are flagged, not counted.
+__global__ void row_count_kernel(const uint32_t* __restrict__ rows, uint64_t nnz, uint32_t m,
+                                 uint32_t* __restrict__ counts, uint32_t* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const uint32_t r = rows[k];
+    const unsigned active = __activemask();
+    if (r >= m) {
+      atomicOr(err, 1u);
+      continue;
+    }
+    const unsigned peers = __match_any_sync(__activemask() & active, r);
+    if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(counts + r, (unsigned)__popc(peers));
+  }
+}
+
 }  // namespace
+
+// row_prefix (inc/triplet.hpp:82-87): prefix[0..m] = exclusive prefix sums of the row counts.
+int row_prefix(const spmvlab_cuda_coo& a, uint32_t* prefix, Arena& ar) {
+  cudaStream_t s = ar.stream();
+  cudaMemsetAsync(prefix, 0, 4 * ((uint64_t)a.m + 1), s);
+  if (a.nnz) {
+    uint32_t* err = ar.alloc_n<uint32_t>(1);
+    if (!err) return kNoMemory;
+    cudaMemsetAsync(err, 0, 4, s);
+    row_count_kernel<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.row_ind, a.nnz, a.m, prefix, err);
+    uint32_t herr = 0;
+    cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (herr) return kIndexOutOfRange;
+  }
+  exclusive_scan_u32(prefix, prefix, a.m, ar);
+  return check_launch("row_prefix");
+}
 
 // validate, inc/triplet.hpp:42-59: range check, then duplicates via sorted (row << 32 | col).
 int validate_coo(const spmvlab_cuda_coo& a, Arena& ar) {

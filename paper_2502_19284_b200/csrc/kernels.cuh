@@ -75,6 +75,7 @@ int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint
 int curve_keys(int kind, const uint32_t* rows, const uint32_t* cols, uint64_t count, unsigned level,
                uint64_t* keys, cudaStream_t s);
 int validate_coo(const spmvlab_cuda_coo& a, Arena& ar);
+int row_prefix(const spmvlab_cuda_coo& a, uint32_t* prefix, Arena& ar);
 int cache_read(const char* path, spmvlab_cuda_coo* a, cudaStream_t s);
 int cache_info(const char* path, uint32_t* m, uint32_t* n, uint64_t* nnz);
 int cache_write(const char* path, const spmvlab_cuda_coo& a, cudaStream_t s);

@@ -223,6 +223,15 @@ def build_format(alg, a: TripletMatrix, threads: int = 1, opt: EngineOptions | N
     return BuiltFormat(h.value, alg)
 
 
+def row_prefix(a: TripletMatrix, stream=None) -> torch.Tensor:
+    """row_counts + row_prefix (inc/triplet.hpp:75-87) on the device: m + 1 exclusive prefix sums
+    (int32-typed u32)."""
+    out = torch.empty(a.m + 1, dtype=torch.int32, device="cuda")
+    coo = a._c()
+    _check(capi.load().spmvlab_cuda_row_prefix(C.byref(coo), out.data_ptr(), _stream(stream)))
+    return out
+
+
 def build_format_beta(alg, a: TripletMatrix, log2_beta: int, threads: int = 1, stream=None) -> BuiltFormat:
     """The per-format builders with an explicit block size 2^log2_beta: build_csb (inc/csb.hpp:51),
     build_mergeb (inc/mergeb.hpp:50), build_bcoh with p = threads bands (inc/bcoh.hpp:194)."""
