@@ -9,9 +9,11 @@ resident in HBM; `value` = 2 nnz K / t  (GFLOP/s).  Inputs (866 MB of algorithmi
 larger than the 126 MB L2, so no flush is needed between steps.
 
 N > 1 (torchrun, one process per GPU): the same matrix is row-sharded by nonzeros across ranks
-(partition_rows_by_nnz with beta = 1, inc/block_size.hpp:73-102); a step is the local multiply
-y_r = A_r x followed by the all-gather of the y_r slices over NCCL (the iterated-SpMV exchange);
-time is the max over ranks; scaling "strong".
+(partition_rows_by_nnz with beta = 1, inc/block_size.hpp:73-102); a step is x_next = A x on every
+rank: the local multiply whose epilogue stores each finished row into every rank's next x (CUDA
+IPC peer stores; --exchange nccl: the local multiply followed by an NCCL all-gatherv of the y_r
+slices), then a stream-ordered rendezvous; time is the max over ranks; scaling "strong";
+"multi_gpu" reports the shard multiply alone beside the step (compute vs exchange).
 
 Extra keys: e2e (host buffers through the C ABI, copies timed), roofline (dominant kernel,
 event-timed in the library), cpu_baseline (the reference's own engine on the host cores),
@@ -392,6 +394,28 @@ def main():
     ms_step = elapsed_ms / args.steps
     value = 2.0 * nnz_total * args.steps / (elapsed_ms / 1e3) / 1e9
 
+    # N > 1: per-step compute (the shard's multiply alone, no exchange) beside the
+    # whole step, max over ranks; exchange = the difference
+    multi_gpu = None
+    if world > 1:
+        import torch.distributed as dist
+        y_only = torch.empty(m_loc, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_only, p=1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_only, p=1)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        comp = float(tt[0]) / args.steps
+        multi_gpu = {"compute_ms_per_step": comp, "exchange_ms_per_step": max(0.0, ms_step - comp),
+                     "note": "compute = the rank's shard multiply alone (max over ranks); exchange = step - compute"}
+        del y_only
+
     # dominant kernel roofline (per launch, this rank)
     rep = sp.storage_report(fmt)
     alg_bytes = rep.total() + 8 * n + 8 * m_loc
@@ -497,6 +521,8 @@ def main():
                            "l2": "inputs larger than L2 (no flush)", "conversion_ms": conv_ms},
                 "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clk,
                 "gpu_launches": launches, "formats": formats, "iterate": iterate}
+        if multi_gpu is not None:
+            line["multi_gpu"] = multi_gpu
         print(json.dumps(line), flush=True)
     if fused is not None:
         fused.close()  # collective

@@ -37,3 +37,5 @@ def test_bench_two_ranks(cuda, exchange):
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 5
     assert d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
     assert d["config"]["exchange"].startswith("fused" if exchange == "fused" else "NCCL")
+    mg = d["multi_gpu"]
+    assert mg["compute_ms_per_step"] > 0 and mg["exchange_ms_per_step"] >= 0
