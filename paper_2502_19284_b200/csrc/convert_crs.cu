@@ -6,8 +6,10 @@
 // the key, gathers data through the permutation and histograms rows (warp-aggregated atomics over
 // the sorted, hence run-grouped, rows), and a decoupled look-back scan for row_ptr.  Keys are
 // unique, so the order -- and every output array -- is bit-identical to the reference's.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -49,9 +51,11 @@ __global__ void crs_populate(const uint64_t* __restrict__ skeys, const uint64_t*
 
 // One merge-path diagonal per tile boundary (diagonal_search, spmv_parallel.hpp:47-69, with
 // A = row_ptr[1..m], B = 0..nnz-1).
+// row_ptr may be a panel's slice of the stacked panel row pointer (first entry `base`); the tile
+// coordinates are then absolute element indices into the panel arrays.
 __global__ void merge_partition(const uint32_t* __restrict__ row_ptr, uint32_t m, uint64_t nnz,
                                 uint32_t tiles, uint32_t tile_items, uint32_t* __restrict__ trow,
-                                uint32_t* __restrict__ tnnz) {
+                                uint32_t* __restrict__ tnnz, uint32_t base = 0) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > tiles) return;
   const uint64_t total = (uint64_t)m + nnz;
@@ -61,10 +65,79 @@ __global__ void merge_partition(const uint32_t* __restrict__ row_ptr, uint32_t m
   uint64_t hi = diag < m ? diag : m;
   while (lo < hi) {
     const uint64_t mid = lo + (hi - lo + 1) / 2;
-    if ((uint64_t)row_ptr[mid] <= diag - mid) lo = mid; else hi = mid - 1;
+    if ((uint64_t)(row_ptr[mid] - base) <= diag - mid) lo = mid; else hi = mid - 1;
   }
   trow[t] = (uint32_t)lo;
-  tnnz[t] = (uint32_t)(diag - lo);
+  tnnz[t] = base + (uint32_t)(diag - lo);
+}
+
+// ---- column panels (merge-CSR when x exceeds the L2): panel k holds the entries with column in
+// [k*W, (k+1)*W), rows in CRS order, stored as the CRS of the K*m-row stacked matrix
+// [A_0; A_1; ...].  Columns are sorted inside a CRS row, so a row's panel split points are binary
+// searches in its col_ind slice.
+__device__ __forceinline__ uint32_t row_lower_bound(const uint32_t* __restrict__ col, uint32_t b, uint32_t e,
+                                                    uint64_t v) {
+  while (b < e) {
+    const uint32_t mid = b + (e - b) / 2;
+    if ((uint64_t)col[mid] < v) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+__global__ void panel_counts(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t m,
+                             uint32_t panels, uint32_t width, uint32_t* __restrict__ cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += stride) {
+    const uint32_t b = row_ptr[r], e = row_ptr[r + 1];
+    uint32_t prev = b;
+    for (uint32_t k = 1; k < panels; ++k) {
+      const uint32_t sp = row_lower_bound(col, prev, e, (uint64_t)k * width);
+      cnt[(uint64_t)(k - 1) * m + r] = sp - prev;
+      prev = sp;
+    }
+    cnt[(uint64_t)(panels - 1) * m + r] = e - prev;
+  }
+}
+
+// Element i of row r in panel k goes to prp[k*m + r] + (i - first element of row r in panel k).
+// One warp per 1024 consecutive elements (coalesced reads; K sequential write streams); an
+// element's row is a binary search of row_ptr between the rows of the chunk's first and last
+// elements, so rows of 10^6 entries (cfg3) are spread over many warps.
+__device__ __forceinline__ uint32_t row_of(const uint32_t* __restrict__ row_ptr, uint32_t lo, uint32_t hi,
+                                           uint32_t i) {
+  // largest r in [lo, hi] with row_ptr[r] <= i
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo + 1) / 2;
+    if (row_ptr[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void panel_fill(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                           const double* __restrict__ val, uint32_t m, uint64_t nnz, uint32_t panels,
+                           uint32_t width, const uint32_t* __restrict__ prp, uint32_t* __restrict__ pcol,
+                           double* __restrict__ pval) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t e0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 1024; e0 < nnz;
+       e0 += wstride * 1024) {
+    const uint32_t e1 = (uint32_t)(e0 + 1024 < nnz ? e0 + 1024 : nnz);
+    uint32_t r_lo = 0, r_hi = 0;
+    if (lane == 0) r_lo = row_of(row_ptr, 0, m - 1, (uint32_t)e0);
+    if (lane == 1) r_hi = row_of(row_ptr, 0, m - 1, e1 - 1);
+    r_lo = __shfl_sync(0xFFFFFFFFu, r_lo, 0);
+    r_hi = __shfl_sync(0xFFFFFFFFu, r_hi, 1);
+    for (uint32_t i = (uint32_t)e0 + lane; i < e1; i += 32) {
+      const uint32_t r = row_of(row_ptr, r_lo, r_hi, i);
+      const uint32_t c = col[i];
+      const uint32_t k = c / width;
+      uint32_t before = 0;  // entries of row r in panels < k
+      for (uint32_t q = 0; q < k; ++q) before += prp[(uint64_t)q * m + r + 1] - prp[(uint64_t)q * m + r];
+      const uint32_t o = prp[(uint64_t)k * m + r] + (i - row_ptr[r] - before);
+      pcol[o] = c;
+      pval[o] = val[i];
+    }
+  }
 }
 
 __global__ void merge_path_search_kernel(const uint32_t* __restrict__ a, uint64_t a_len,
@@ -155,15 +228,59 @@ int build_merge_plan(Format& f, Arena& ar) {
   f.merge_ipt = ipt;
   f.merge_variant = var;
   const uint32_t tile_items = merge_tile_items(th, ipt, var);
-  const uint64_t tiles = (total + tile_items - 1) / tile_items;
+  // Column panels for the merge engine when x outgrows the L2 (beyond ~L2 the x
+  // gathers become DRAM sectors): K = ceil(8n / kPanelXBytes), at most kMaxMergePanels, so each
+  // panel's x window stays L2-resident while its slice of A streams past.
+  uint32_t panels = 1;
+  if (f.alg == kMerge && (var == kVariantVector || var == kVariantVector3) && f.nnz > 0) {
+    const uint64_t xb = 8ull * f.n;
+    panels = (uint32_t)std::min<uint64_t>(kMaxMergePanels, (xb + kPanelXBytes - 1) / kPanelXBytes);
+    if (const char* e = getenv("SPMVLAB_MERGE_PANELS")) panels = (uint32_t)std::max(1, std::min(atoi(e), kMaxMergePanels));
+    if ((uint64_t)panels * f.m + 1 > 0xFFFFFFFFull || f.n < panels) panels = 1;
+  }
+  f.merge_panels = panels;
+  f.merge_panel_width = panels > 1 ? (f.n + panels - 1) / panels : f.n;
+  std::vector<uint32_t> pbase(panels + 1, 0);
+  const uint32_t* prp = nullptr;
+  if (panels > 1) {
+    const uint64_t rows = (uint64_t)panels * f.m;
+    uint32_t* p_rp = static_cast<uint32_t*>(f.add("merge_panel_row_ptr", rows + 1, 4, s));
+    uint32_t* p_col = static_cast<uint32_t*>(f.add("merge_panel_col", f.nnz, 4, s));
+    double* p_val = static_cast<double*>(f.add("merge_panel_data", f.nnz, 8, s));
+    if (!p_rp || !p_col || !p_val) return kNoMemory;
+    const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
+    const uint32_t* col = f.find("col_ind")->as<uint32_t>();
+    panel_counts<<<grid_for(f.m, 256), 256, 0, s>>>(rp, col, f.m, panels, f.merge_panel_width, p_rp);
+    exclusive_scan_u32(p_rp, p_rp, rows, ar);
+    panel_fill<<<grid_for((f.nnz + 1023) / 1024 * 32, 256), 256, 0, s>>>(
+        rp, col, f.find("data")->as<double>(), f.m, f.nnz, panels, f.merge_panel_width, p_rp, p_col, p_val);
+    for (uint32_t k = 0; k <= panels; ++k)
+      cudaMemcpyAsync(&pbase[k], p_rp + (uint64_t)k * f.m, 4, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan (panels)");
+    prp = p_rp;
+  } else {
+    pbase[1] = (uint32_t)f.nnz;
+  }
+  f.panel_tile_off.assign(panels + 1, 0);
+  for (uint32_t k = 0; k < panels; ++k) {
+    const uint64_t tk = ((uint64_t)f.m + (pbase[k + 1] - pbase[k]) + tile_items - 1) / tile_items;
+    f.panel_tile_off[k + 1] = f.panel_tile_off[k] + (uint32_t)tk;
+  }
+  const uint64_t tiles = f.panel_tile_off[panels];
   f.merge_tiles = (uint32_t)tiles;
-  uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + 1, 4, s));
-  uint32_t* tnnz = static_cast<uint32_t*>(f.add("merge_tile_nnz", tiles + 1, 4, s));
+  // one extra coordinate per panel (each panel's tile list has tiles_k + 1 boundaries)
+  uint32_t* trow = static_cast<uint32_t*>(f.add("merge_tile_row", tiles + panels, 4, s));
+  uint32_t* tnnz = static_cast<uint32_t*>(f.add("merge_tile_nnz", tiles + panels, 4, s));
   if (!trow || !tnnz) return kNoMemory;
   // carry scratch is per stream (Format::stream_scratch); pre-create the build stream's
   if (!f.stream_scratch(s)) return kNoMemory;
-  merge_partition<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, s>>>(
-      f.find("row_ptr")->as<uint32_t>(), f.m, f.nnz, (uint32_t)tiles, tile_items, trow, tnnz);
+  for (uint32_t k = 0; k < panels; ++k) {
+    const uint32_t tk = f.panel_tile_off[k + 1] - f.panel_tile_off[k];
+    const uint32_t o = f.panel_tile_off[k] + k;
+    merge_partition<<<(unsigned)((tk + 1 + 255) / 256), 256, 0, s>>>(
+        panels > 1 ? prp + (uint64_t)k * f.m : f.find("row_ptr")->as<uint32_t>(), f.m,
+        (uint64_t)(pbase[k + 1] - pbase[k]), tk, tile_items, trow + o, tnnz + o, pbase[k]);
+  }
   // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32]; rows longer
   // than kParLongIters * width get one CTA each.  On heavy-tailed row lengths (more than 0.1 % of
   // the rows are "long") many narrow groups plus the per-row CTAs win instead: width 2, CTAs above

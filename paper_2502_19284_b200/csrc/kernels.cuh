@@ -27,6 +27,10 @@ constexpr int kMergeVariant = kVariantVector;
 // ParCRS: rows longer than kParLongIters * group width are summed by a whole CTA (a sub-warp group
 // would walk them serially -- R-MAT s22 row 0 has ~10^5 nonzeros); those CTAs come first in the grid.
 constexpr uint32_t kParLongIters = 32;
+// Column panels of the merge engine: one panel per kPanelXBytes of x (at most kMaxMergePanels);
+// the B200 L2 is 126 MB, so x up to 96 MB runs unpanelled (R-MAT s22: 33.5 MB).
+constexpr int kMaxMergePanels = 4;
+constexpr uint64_t kPanelXBytes = 96ull << 20;
 bool merge_shape_supported(int threads, int ipt, int variant);
 uint32_t merge_tile_items(int threads, int ipt, int variant);
 

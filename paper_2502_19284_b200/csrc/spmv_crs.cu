@@ -592,7 +592,16 @@ __device__ __forceinline__ void vec_products_c(const uint32_t* __restrict__ col,
 // row_ptr and scattered to the element they close (smap: element -> row + 1); each lane
 // then walks its 4 products in registers, stores rows that close inside the lane, and the lane
 // tails are combined by one warp segmented scan (carry = the open row's running sum).
-template <bool SCATTER>
+// ACC (column panels after the first): finished rows are added to y (the earlier panels' sums)
+// instead of stored; rows with no entries in the panel are left alone unless they must also be
+// scattered to the peers (the last panel of the fused exchange stores every row's final value).
+template <bool SCATTER, bool ACC>
+__device__ __forceinline__ void put_row_m(double* y, const RowDest& d, uint32_t r, double v) {
+  if constexpr (ACC) v += y[r];
+  put_row<SCATTER>(y, d, r, v);
+}
+
+template <bool SCATTER, bool ACC>
 __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, double* __restrict__ y, uint32_t* smap,
                                          uint32_t base, uint32_t j0, uint32_t j1, uint32_t r1, uint32_t& rp,
                                          uint32_t& prevE, const double p[4], double& carry, unsigned lane,
@@ -607,7 +616,9 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
     if (lane == 0) S = prevE;
     const bool in = have && E <= pend;
     if (in) {
-      if (E == S || E <= j0) put_row<SCATTER>(y, dest, idx, 0.0);  // empty, or elements precede the tile
+      if (E == S || E <= j0) {  // empty, or elements precede the tile
+        if (!ACC || SCATTER) put_row_m<SCATTER, ACC>(y, dest, idx, 0.0);
+      }
       else smap[E - 1 - base] = idx + 1u;   // closes at element E - 1 of this pass
     }
     const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
@@ -632,7 +643,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
         first_row = rid[u];
         first_val = run;
       } else {
-        put_row<SCATTER>(y, dest, rid[u], run);
+        put_row_m<SCATTER, ACC>(y, dest, rid[u], run);
       }
       run = 0.0;
     }
@@ -651,7 +662,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
   if (lane == 0) ex = 0.0;
   if (first_row >= 0)
-    put_row<SCATTER>(y, dest, first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
+    put_row_m<SCATTER, ACC>(y, dest, first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
   const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
   carry = heads ? v31 : carry + v31;
   __syncwarp();
@@ -660,7 +671,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
 // Merge-path tiles of 32 * IPT items per warp (the same partition and carry fix-up as the other
 // variants), the tile's elements walked in lane-blocked passes of 128 with two passes' loads and
 // gathers in flight.  No product staging: shared memory holds only the 128-entry row map.
-template <int IPT, int WARPS, int NP, bool SCATTER>
+template <int IPT, int WARPS, int NP, bool SCATTER, bool ACC>
 __global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
@@ -704,7 +715,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NP == 1 ? 40 : 48) / WARPS) merge
         more = false;
         break;
       }
-      vec_pass<SCATTER>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane, dest);
+      vec_pass<SCATTER, ACC>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane, dest);
     }
     if (!(base + 128u * NPP < j1 || rp < r1)) more = false;
   }
@@ -896,15 +907,33 @@ void launch_merge_wstage(const Format& f, const double* x, double* y, const Scra
                                                                                                f.merge_tiles);
 }
 
+// Panel k of a column-panelled format (k = 0 and one panel: the plain CRS arrays).  The fix-up of
+// panel k runs before panel k + 1's kernel (stream order; PDL waits for full completion), so the
+// accumulating panels read final sums.
 template <int THREADS, int IPT, int NP>
 void launch_merge_vec(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
-                      const RowDest& dest) {
+                      const RowDest& dest, uint32_t k) {
   constexpr int WARPS = THREADS / 32;
-  const unsigned grid = (f.merge_tiles + WARPS - 1) / WARPS;
-  if (dest.n)
-    launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, true>, grid, THREADS, s, MERGE_ARGS, f.merge_tiles, dest);
-  else
-    launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, false>, grid, THREADS, s, MERGE_ARGS, f.merge_tiles, dest);
+  const uint32_t t0 = f.panel_tile_off[k], tiles = f.panel_tile_off[k + 1] - t0, o = t0 + k;
+  if (tiles == 0) return;
+  const unsigned grid = (tiles + WARPS - 1) / WARPS;
+  const bool pan = f.merge_panels > 1;
+  const uint32_t* rp = pan ? f.find("merge_panel_row_ptr")->as<uint32_t>() + (uint64_t)k * f.m
+                           : f.find("row_ptr")->as<uint32_t>();
+  const uint32_t* col = f.find(pan ? "merge_panel_col" : "col_ind")->as<uint32_t>();
+  const double* val = f.find(pan ? "merge_panel_data" : "data")->as<double>();
+  const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>() + o;
+  const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>() + o;
+#define MERGE_VEC_ARGS rp, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest
+  const bool scatter = dest.n && k + 1 == f.merge_panels;
+  if (k == 0) {
+    if (scatter) launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, true, false>, grid, THREADS, s, MERGE_VEC_ARGS);
+    else launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, false, false>, grid, THREADS, s, MERGE_VEC_ARGS);
+  } else {
+    if (scatter) launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, true, true>, grid, THREADS, s, MERGE_VEC_ARGS);
+    else launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, NP, false, true>, grid, THREADS, s, MERGE_VEC_ARGS);
+  }
+#undef MERGE_VEC_ARGS
 }
 
 template <int THREADS, int IPT>
@@ -995,11 +1024,11 @@ static const char* merge_kernel_name(int variant) {
 
 template <int T, int I, int V>
 static void launch_merge_shape(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
-                               const RowDest& dest) {
+                               const RowDest& dest, uint32_t k) {
   if constexpr (V == kVariantShuffle) launch_merge_shfl<T, I>(f, x, y, sc, s);
   else if constexpr (V == kVariantWarpStage) launch_merge_wstage<T, I>(f, x, y, sc, s);
-  else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s, dest);
-  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 1>(f, x, y, sc, s, dest);  // col prefetch
+  else if constexpr (V == kVariantVector) launch_merge_vec<T, I, 2>(f, x, y, sc, s, dest, k);
+  else if constexpr (V == kVariantVector3) launch_merge_vec<T, I, 1>(f, x, y, sc, s, dest, k);  // col prefetch
   else if constexpr (V == kVariantSmem) launch_merge_smem<T, I>(f, x, y, sc, s);
   else launch_merge_tma<T, I, 2>(f, x, y, sc, s);
 }
@@ -1024,31 +1053,36 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
     g_last_error = "device allocation failed (merge carry scratch)";
     return kNoMemory;
   }
-  bool launched = false;
+  const bool vec = variant == kVariantVector || variant == kVariantVector3;
+  // with column panels the timed region spans every panel's kernel and the fix-ups between them
   timing_begin(merge_kernel_name(variant), s);
+  for (uint32_t k = 0; k < f.merge_panels; ++k) {
+    bool launched = false;
 #define SPMV_MERGE_SHAPE(T, I, V)                              \
   if (!launched && threads == T && ipt == I && variant == V) { \
-    launch_merge_shape<T, I, V>(f, x, y, sc, s, dest);         \
+    launch_merge_shape<T, I, V>(f, x, y, sc, s, dest, k);      \
     launched = true;                                           \
   }
 #include "merge_shapes.inc"
 #undef SPMV_MERGE_SHAPE
-  timing_end(s);
-  if (!launched) {
-    g_last_error = "merge tile shape not instantiated";
-    return kInvalidArgument;
+    if (k + 1 == f.merge_panels) timing_end(s);
+    if (!launched) {
+      g_last_error = "merge tile shape not instantiated";
+      return kInvalidArgument;
+    }
+    note_launch(2);
+    const uint32_t t0 = f.panel_tile_off[k], tiles = f.panel_tile_off[k + 1] - t0;
+    const uint32_t* crow = sc->carry_row + t0;
+    const double* cval = sc->carry_val + t0;
+    const unsigned fgrid = (tiles + 255) / 256;
+    if (tiles == 0) continue;
+    if (dest.n && k + 1 == f.merge_panels)
+      launch_pdl(merge_fixup_kernel<true>, fgrid, 256, s, crow, cval, tiles, y, f.m, dest);
+    else if (vec)
+      launch_pdl(merge_fixup_kernel<false>, fgrid, 256, s, crow, cval, tiles, y, f.m, dest);
+    else
+      merge_fixup_kernel<false><<<fgrid, 256, 0, s>>>(crow, cval, tiles, y, f.m, dest);
   }
-  note_launch(2);
-  const unsigned fgrid = (f.merge_tiles + 255) / 256;
-  const bool vec = variant == kVariantVector || variant == kVariantVector3;
-  if (dest.n)
-    launch_pdl(merge_fixup_kernel<true>, fgrid, 256, s, (const uint32_t*)sc->carry_row, (const double*)sc->carry_val,
-               f.merge_tiles, y, f.m, dest);
-  else if (vec)
-    launch_pdl(merge_fixup_kernel<false>, fgrid, 256, s, (const uint32_t*)sc->carry_row, (const double*)sc->carry_val,
-               f.merge_tiles, y, f.m, dest);
-  else
-    merge_fixup_kernel<false><<<fgrid, 256, 0, s>>>(sc->carry_row, sc->carry_val, f.merge_tiles, y, f.m, dest);
   return check_launch("spmv_merge");
 }
 

@@ -166,7 +166,8 @@ class StorageBreakdown:
 
 
 _DT = {"data": np.float64, "row_jump_block": np.int16, "col_jump_block": np.int16,
-       "col_inc": np.uint16, "row_jump": np.uint16, "merge_carry_val": np.float64}
+       "col_inc": np.uint16, "row_jump": np.uint16, "merge_carry_val": np.float64,
+       "merge_panel_data": np.float64}
 _U64 = {"off_elem", "off_block", "off_row_jump_block", "off_blk_ptr", "off_row_jump"}
 
 
