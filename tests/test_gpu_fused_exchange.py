@@ -58,7 +58,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_fused_exchange_two_ranks_match_oracle(cuda, oracle):
+@pytest.mark.parametrize("panels", [None, 3])
+def test_fused_exchange_two_ranks_match_oracle(cuda, oracle, monkeypatch, panels):
+    """panels=3: the column-panelled merge engine (only the last panel scatters; rows empty in it
+    must still reach the peers)."""
+    if panels:
+        monkeypatch.setenv("SPMVLAB_MERGE_PANELS", str(panels))  # inherited by the spawned ranks
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -86,15 +91,22 @@ def test_fused_exchange_two_ranks_match_oracle(cuda, oracle):
     assert all(p.exitcode == 0 for p in procs)
 
 
-def test_scatter_single_rank_equals_run_spmv(cuda):
+@pytest.mark.parametrize("panels", [None, 2, 4])
+def test_scatter_single_rank_equals_run_spmv(cuda, monkeypatch, panels):
     """World 1: the scatter multiply with no peers is the plain merge multiply (bitwise), and a
-    destination list copies every row (including rows finished by the carry fix-up)."""
+    destination list copies every row (including rows finished by the carry fix-up), also with
+    column panels."""
     sp = cuda
     import ctypes as C
     from paper_2502_19284_b200 import capi, gen
     from paper_2502_19284_b200.engine import _check
     m, n, r, c, v = gen.rmat_host(12, 16, seed=2)
+    if panels:
+        monkeypatch.setenv("SPMVLAB_MERGE_PANELS", str(panels))
     f = sp.build_format(2, sp.TripletMatrix.from_host(m, n, r, c, v), 1)
+    if panels:
+        monkeypatch.delenv("SPMVLAB_MERGE_PANELS")
+        assert len(f.array("merge_panel_row_ptr")) == panels * m + 1
     x = torch.rand(n, dtype=torch.float64, device="cuda")
     y_ref = sp.run_spmv(2, f, x)
     y = torch.empty(m, dtype=torch.float64, device="cuda")
