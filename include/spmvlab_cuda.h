@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define SPMVLAB_CUDA_ABI_VERSION 1
+#define SPMVLAB_CUDA_ABI_VERSION 2
 
 /* Opaque, device-resident, immutable format (a BuiltFormat, inc/engine.hpp:82). */
 typedef struct spmvlab_cuda_format spmvlab_cuda_format;
@@ -62,10 +62,16 @@ typedef struct {
   uint32_t log2_beta, block_rows, block_cols;
   uint32_t element_level, block_level, bands;
   uint32_t merge_tiles, work_items;
+  uint32_t merge_ipt, merge_panels; /* merge-CSR warp tile = 32 * merge_ipt items; column panels */
 } spmvlab_cuda_format_info;
 
 int spmvlab_cuda_abi_version(void);
 const char* spmvlab_cuda_last_error(void);
+
+/* Returns the free blocks the library keeps in the device's stream-ordered pool (conversion scratch
+ * is kept between builds) to the driver, e.g. before another allocator needs the memory.  No
+ * reference counterpart (the reference's scratch is std::vector). */
+int spmvlab_cuda_release_pool(void);
 
 /* build_format(Algorithm, const TripletMatrix&, threads, EngineOptions)  -- inc/engine.hpp:96-122.
  * `threads` is the BCOH band count p (inc/engine.hpp:108-115), ignored by the other formats. */

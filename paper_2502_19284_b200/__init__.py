@@ -10,6 +10,6 @@ from .engine import (  # noqa: F401
     IncrementalRowStorage, bicrs_from_arrays, crs_to_icrs, triplet_to_bicrs,
     CSB_ITEM_DTYPE, csb_items_numpy, csb_work_items,
     format_to_triplet, crs_to_triplet, csb_to_triplet, bcoh_to_triplet, mergeb_to_triplet,
-    engine_block_size, exclusive_scan, iterate, merge_path_search, partition_rows_by_nnz, run_spmv,
+    engine_block_size, exclusive_scan, iterate, merge_path_search, partition_rows_by_nnz, release_cached_memory, run_spmv,
     run_spmv_host, select_block_size, sort_pairs, storage_report, validate,
 )

@@ -12,9 +12,11 @@ from .build import LIB
 
 _lib = None
 
+ABI_VERSION = 2  # SPMVLAB_CUDA_ABI_VERSION of include/spmvlab_cuda.h
+
 # Every symbol include/spmvlab_cuda.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = [
-    "spmvlab_cuda_abi_version", "spmvlab_cuda_last_error", "spmvlab_cuda_build_format",
+    "spmvlab_cuda_abi_version", "spmvlab_cuda_last_error", "spmvlab_cuda_release_pool", "spmvlab_cuda_build_format",
     "spmvlab_cuda_run_spmv", "spmvlab_cuda_run_spmv_host", "spmvlab_cuda_storage_report",
     "spmvlab_cuda_get_format_info", "spmvlab_cuda_format_array", "spmvlab_cuda_download_array",
     "spmvlab_cuda_free_format", "spmvlab_cuda_validate", "spmvlab_cuda_select_block_size",
@@ -64,7 +66,8 @@ class FormatInfo(C.Structure):
     _fields_ = [("alg", C.c_int), ("m", C.c_uint32), ("n", C.c_uint32), ("nnz", C.c_uint64),
                 ("log2_beta", C.c_uint32), ("block_rows", C.c_uint32), ("block_cols", C.c_uint32),
                 ("element_level", C.c_uint32), ("block_level", C.c_uint32), ("bands", C.c_uint32),
-                ("merge_tiles", C.c_uint32), ("work_items", C.c_uint32)]
+                ("merge_tiles", C.c_uint32), ("work_items", C.c_uint32),
+                ("merge_ipt", C.c_uint32), ("merge_panels", C.c_uint32)]
 
 
 def lib_path() -> str:
@@ -129,5 +132,8 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_free_coo.argtypes = [C.POINTER(Coo)]
     L.spmvlab_cuda_free_coo.restype = None
     L.spmvlab_cuda_cache_info.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]
+    if L.spmvlab_cuda_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{LIB} has ABI {L.spmvlab_cuda_abi_version()}, this package needs {ABI_VERSION} "
+                           "(stale build: run __graft_entry__.build())")
     _lib = L
     return L

@@ -178,11 +178,8 @@ void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t
   // does not pay the driver's page mapping again); build_format synchronises its stream before
   // returning, so the arrays are then usable from any stream.  Released with cudaFree.
   const uint64_t alloc = ((a.bytes + 15) & ~uint64_t(15)) + 64;
-  pool_init();
-  if (cudaMallocAsync(&a.ptr, alloc, s) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
+  a.ptr = pool_alloc(alloc, s);
+  if (!a.ptr) return nullptr;
   arrays.push_back(a);
   return a.ptr;
 }
@@ -198,6 +195,11 @@ extern "C" {
 int spmvlab_cuda_abi_version(void) { return SPMVLAB_CUDA_ABI_VERSION; }
 
 const char* spmvlab_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int spmvlab_cuda_release_pool(void) {
+  pool_trim();
+  return check_launch("spmvlab_cuda_release_pool");
+}
 
 unsigned spmvlab_cuda_select_block_size(uint64_t n, unsigned cap, uint64_t l2_bytes) {
   return select_block_size(n, cap, l2_bytes);
@@ -438,6 +440,8 @@ int spmvlab_cuda_get_format_info(const spmvlab_cuda_format* f, spmvlab_cuda_form
   info->bands = f->bands;
   info->merge_tiles = f->merge_tiles;
   info->work_items = f->work_items;
+  info->merge_ipt = f->merge_ipt;
+  info->merge_panels = f->merge_panels;
   return kOk;
 }
 

@@ -211,28 +211,23 @@ int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar) {
 int build_merge_plan(Format& f, Arena& ar) {
   cudaStream_t s = ar.stream();
   const uint64_t total = (uint64_t)f.m + f.nnz;
-  int th = kMergeThreads, ipt = kMergeIpt, var = kMergeVariant;
+  int ipt = kMergeIpt;
   // tile size: the largest of 32 / 16 / 8 items per lane that still leaves >= 4 warp tiles per
   // resident warp slot (148 SMs x 48 warps), so small matrices keep every SM busy
   const uint64_t slots = 4ull * kNumSMs * 48;
   ipt = total >= slots * 32 * 32 ? 32 : (total >= slots * 32 * 16 ? 16 : 8);
-  if (const char* e = getenv("SPMVLAB_MERGE_CFG")) {  // developer override "threads,ipt,variant"
-    int a = 0, b = 0, c = 0;
-    if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && merge_shape_supported(a, b, c)) {
-      th = a;
-      ipt = b;
-      var = c;
-    }
+  if (const char* e = getenv("SPMVLAB_MERGE_IPT")) {  // developer / test override: 8, 16 or 32
+    const int v = atoi(e);
+    if (merge_shape_supported(kMergeThreads, v)) ipt = v;
   }
-  f.merge_threads = th;
+  f.merge_threads = kMergeThreads;
   f.merge_ipt = ipt;
-  f.merge_variant = var;
-  const uint32_t tile_items = merge_tile_items(th, ipt, var);
+  const uint32_t tile_items = 32u * (uint32_t)ipt;
   // Column panels for the merge engine when x outgrows the L2 (beyond ~L2 the x
   // gathers become DRAM sectors): K = ceil(8n / kPanelXBytes), at most kMaxMergePanels, so each
   // panel's x window stays L2-resident while its slice of A streams past.
   uint32_t panels = 1;
-  if (f.alg == kMerge && (var == kVariantVector || var == kVariantVector3) && f.nnz > 0) {
+  if (f.alg == kMerge && f.nnz > 0) {
     const uint64_t xb = 8ull * f.n;
     panels = (uint32_t)std::min<uint64_t>(kMaxMergePanels, (xb + kPanelXBytes - 1) / kPanelXBytes);
     if (const char* e = getenv("SPMVLAB_MERGE_PANELS")) panels = (uint32_t)std::max(1, std::min(atoi(e), kMaxMergePanels));

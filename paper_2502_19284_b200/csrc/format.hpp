@@ -37,7 +37,7 @@ struct spmvlab_cuda_format {
 
   // ---- merge-path plan (CRS formats), spmv_parallel.hpp:82-86 at tile granularity
   uint32_t merge_tiles = 0;
-  uint32_t merge_threads = 256, merge_ipt = 7, merge_variant = 0;  // tile = threads * ipt items
+  uint32_t merge_threads = 256, merge_ipt = 32;  // warp tile = 32 * ipt merge items
   // column panels (merge engine, x larger than the L2): panel k = columns [k*W, (k+1)*W), its
   // tiles at merge_tile_row/nnz[panel_tile_off[k] + k ...], carries at [panel_tile_off[k] ...]
   uint32_t merge_panels = 1, merge_panel_width = 0;

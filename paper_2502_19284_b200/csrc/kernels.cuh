@@ -12,18 +12,10 @@
 
 namespace spmvcu {
 
-// merge-CSR tile kernels (spmv_crs.cu) and the default shape.  For kVariantShuffle a tile is one
-// warp's 32 * ipt merge items (ipt = groups of 32 nonzeros in flight per lane); for the others a
-// tile is threads * ipt items of one CTA.
-constexpr int kVariantSmem = 0;
-constexpr int kVariantTma = 1;
-constexpr int kVariantShuffle = 2;
-constexpr int kVariantWarpStage = 3;
-constexpr int kVariantVector = 4;   // lane-blocked passes, two passes in flight
-constexpr int kVariantVector3 = 5;  // the same, next pass's col_ind quad prefetched
+// merge-CSR tile kernel (spmv_crs.cu): one warp tile of 32 * ipt merge items, ipt picked from
+// {32, 16, 8} by matrix size at build time (256 threads per CTA).
 constexpr int kMergeThreads = 256;
-constexpr int kMergeIpt = 32;  // upper bound; build_merge_plan picks 32 / 16 / 8 by matrix size
-constexpr int kMergeVariant = kVariantVector;
+constexpr int kMergeIpt = 32;
 // ParCRS: rows longer than kParLongIters * group width are summed by a whole CTA (a sub-warp group
 // would walk them serially -- R-MAT s22 row 0 has ~10^5 nonzeros); those CTAs come first in the grid.
 constexpr uint32_t kParLongIters = 32;
@@ -31,8 +23,7 @@ constexpr uint32_t kParLongIters = 32;
 // the B200 L2 is 126 MB, so x up to 96 MB runs unpanelled (R-MAT s22: 33.5 MB).
 constexpr int kMaxMergePanels = 4;
 constexpr uint64_t kPanelXBytes = 96ull << 20;
-bool merge_shape_supported(int threads, int ipt, int variant);
-uint32_t merge_tile_items(int threads, int ipt, int variant);
+bool merge_shape_supported(int threads, int ipt);
 
 // ---- conversions (COO -> format); each returns a Status
 int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar);
@@ -51,12 +42,17 @@ struct RowDest {
 };
 // SCATTER = false compiles to the plain store (the destination list is then never touched, so the
 // kernels keep their register / stack budget); kernels take the list as __grid_constant__.
-template <bool SCATTER>
+// LAST = false: the value is a column panel's partial sum that the next panel reads back, so it
+// is stored with the default L2 policy; the final y is written once and leaves with evict-first
+// (keeps the L2 for x: cfg3 / cfg4, x ~ L2 size: -2..3 %).
+template <bool SCATTER, bool LAST = true>
 __device__ __forceinline__ void put_row(double* y, const RowDest& d, uint32_t r, double v) {
-  {  // y is written once: evict-first keeps the L2 for x (cfg3 / cfg4, x ~ L2 size: -2..3 %)
+  if constexpr (LAST) {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(y + r), "d"(v), "l"(pol) : "memory");
+  } else {
+    y[r] = v;
   }
   if constexpr (SCATTER)
     for (unsigned i = 0; i < d.n; ++i) d.p[i][d.off + r] = v;

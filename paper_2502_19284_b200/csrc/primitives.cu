@@ -38,11 +38,32 @@ void pool_init() {
   });
 }
 
-void* Arena::alloc(size_t bytes) {
+void pool_trim() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  cudaDeviceSynchronize();  // frees still in flight on other streams return to the pool first
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+}
+
+// Stream-ordered allocation from the kept pool.  If the device is out of memory, the pool's cached
+// free blocks go back to the driver (another allocator in the process -- torch's -- may need them
+// as much as we do) and the allocation is retried once.
+void* pool_alloc(size_t bytes, cudaStream_t s) {
   pool_init();
   void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) == cudaSuccess) return p;
+  cudaGetLastError();
+  pool_trim();
+  if (cudaMallocAsync(&p, bytes, s) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+void* Arena::alloc(size_t bytes) {
   if (bytes == 0) bytes = 16;
-  if (cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s_) != cudaSuccess) return nullptr;
+  void* p = pool_alloc((bytes + 255) & ~size_t(255), s_);
+  if (!p) return nullptr;
   ptrs_.push_back(p);
   return p;
 }

@@ -15,6 +15,8 @@ namespace spmvcu {
 // Stream-ordered scratch allocations released when the arena dies.
 // Keeps freed device memory in the default stream-ordered pool (release threshold = max).
 void pool_init();
+void pool_trim();                             // return the pool's cached free blocks to the driver
+void* pool_alloc(size_t bytes, cudaStream_t s);  // cudaMallocAsync, trim + retry once when out of memory
 
 class Arena {
  public:

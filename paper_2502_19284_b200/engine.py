@@ -201,6 +201,25 @@ class BuiltFormat:
                                                  C.byref(nbytes)))
         return out
 
+    def array_device(self, name: str) -> torch.Tensor:
+        """Device copy of one named array as a torch tensor (full-size parity checks without a host
+        round trip): float64 for values, int64 for every integer array (unsigned values kept)."""
+        L = capi.load()
+        ptr, nbytes = C.c_void_p(), C.c_uint64()
+        _check(L.spmvlab_cuda_format_array(self._h, name.encode(), C.byref(ptr), C.byref(nbytes)))
+        dt = np.dtype(np.uint64 if name in _U64 else _DT.get(name, np.uint32))
+        count = nbytes.value // dt.itemsize
+        dev = torch.device("cuda", torch.cuda.current_device())
+        torch.cuda.synchronize()
+        if dt == np.float64:
+            return _view_copy(ptr.value, count, "<f8", torch.float64, dev)
+        signed = {1: ("<i1", torch.int8), 2: ("<i2", torch.int16), 4: ("<i4", torch.int32),
+                  8: ("<i8", torch.int64)}[dt.itemsize]
+        t = _view_copy(ptr.value, count, signed[0], signed[1], dev).to(torch.int64)
+        if dt.kind == "u" and dt.itemsize < 8:
+            t &= (1 << (8 * dt.itemsize)) - 1
+        return t
+
     def close(self):
         if self._h:
             try:
@@ -566,6 +585,16 @@ def cache_write(path: str, a: TripletMatrix, stream=None) -> None:
     """Device triplet -> SPMVLAB1 cache, byte-identical to the reference's cache_write."""
     coo = a._c()
     _check(capi.load().spmvlab_cuda_cache_write(str(path).encode(), C.byref(coo), _stream(stream)))
+
+
+def release_cached_memory() -> None:
+    """Returns cached free device memory of both allocators in the process -- the library's stream-
+    ordered pool (conversion scratch kept between builds) and torch's caching allocator -- to the
+    driver, before a phase that needs tens of GB from the other one."""
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    _check(capi.load().spmvlab_cuda_release_pool())
 
 
 def select_block_size(n: int, index_bits_cap: int, l2_bytes: int = DEFAULT_L2_BYTES) -> int:

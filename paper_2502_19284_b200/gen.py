@@ -15,7 +15,9 @@ so these generators stand in for them with the configs' shapes, sizes and value 
         normalize_columns=True)
 
 Input synthesis only (not the hot path): device generators use torch's seeded CUDA RNG, and the
-resulting COO is shuffled so conversions see unordered triplets.
+resulting COO is shuffled so conversions see unordered triplets.  Every reduction is deterministic
+(sorts plus fixed-order segment sums, no floating-point atomics), so two processes -- the two bench
+arms, or a test and its committed fixture -- generate bit-identical matrices from the same seed.
 """
 from __future__ import annotations
 
@@ -101,7 +103,61 @@ def _shuffle(g, *ts):
 
 
 def _as_u32(t: torch.Tensor) -> torch.Tensor:
-    return t.to(torch.int32).contiguous()
+    out = t.to(torch.int32).contiguous()
+    if out.is_cuda:  # the generators' sort temporaries (tens of GB at scale 26) go back to the driver
+        torch.cuda.empty_cache()
+    return out
+
+
+SEG_BLOCK = 32
+
+
+def _short_sums(vals: torch.Tensor, starts: torch.Tensor, lens: torch.Tensor) -> torch.Tensor:
+    """out[i] = vals[starts[i]] + vals[starts[i] + 1] + ... (lens[i] terms, left to right)."""
+    out = torch.zeros(starts.numel(), dtype=vals.dtype, device=vals.device)
+    ne = torch.nonzero(lens > 0).squeeze(1)
+    out[ne] = vals[starts[ne]]
+    act = torch.nonzero(lens > 1).squeeze(1)
+    k = 1
+    while act.numel():
+        out[act] = out[act] + vals[starts[act] + k]
+        k += 1
+        act = act[lens[act] > k]
+    return out
+
+
+def segment_sums(vals: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
+    """Deterministic sums of consecutive segments (counts[i] values each, empty segments give 0):
+    left to right within blocks of SEG_BLOCK values, then the block sums the same way, recursively.
+    A segment of at most SEG_BLOCK values is the plain left-to-right sum."""
+    counts = counts.to(torch.int64)
+    while True:
+        starts = torch.cumsum(counts, 0) - counts
+        if counts.numel() == 0 or int(counts.max()) <= SEG_BLOCK:
+            return _short_sums(vals, starts, counts)
+        npieces = (counts + SEG_BLOCK - 1) // SEG_BLOCK
+        seg = torch.repeat_interleave(torch.arange(counts.numel(), device=counts.device), npieces)
+        first_piece = torch.cumsum(npieces, 0) - npieces
+        within = torch.arange(seg.numel(), device=counts.device) - first_piece[seg]
+        pstart = starts[seg] + within * SEG_BLOCK
+        plen = torch.clamp(counts[seg] - within * SEG_BLOCK, max=SEG_BLOCK)
+        vals = _short_sums(vals, pstart, plen)
+        counts = npieces
+
+
+def sum_duplicates(key: torch.Tensor, vals: torch.Tensor):
+    """(unique sorted keys, summed values): duplicates summed in their original order."""
+    sk, order = torch.sort(key, stable=True)
+    uk, counts = torch.unique_consecutive(sk, return_counts=True)
+    del sk
+    return uk, segment_sums(vals[order], counts)
+
+
+def column_sums(cols: torch.Tensor, vals: torch.Tensor, n: int) -> torch.Tensor:
+    """Deterministic per-column sums (entries of a column in their storage order)."""
+    _, order = torch.sort(cols, stable=True)
+    counts = torch.bincount(cols, minlength=n)
+    return segment_sums(vals[order], counts)
 
 
 def rmat_device(scale: int, edge_factor: int = 16, probs=RMAT_PROBS, seed: int = 1,
@@ -123,17 +179,13 @@ def rmat_device(scale: int, edge_factor: int = 16, probs=RMAT_PROBS, seed: int =
     vals = 1.0 - torch.rand(e, generator=g, device=device, dtype=torch.float64)
     key = rows * n + cols
     del rows, cols
-    uk, inv = torch.unique(key, return_inverse=True)
-    del key
-    sv = torch.zeros(uk.numel(), dtype=torch.float64, device=device)
-    sv.index_add_(0, inv, vals)
-    del inv, vals
+    uk, sv = sum_duplicates(key, vals)
+    del key, vals
     r = uk // n
     cc = uk % n
     del uk
     if normalize_columns:
-        colsum = torch.zeros(n, dtype=torch.float64, device=device)
-        colsum.index_add_(0, cc, sv)
+        colsum = column_sums(cc, sv, n)
         sv = sv / colsum[cc]
     r, cc, sv = _shuffle(g, r, cc, sv)
     return n, n, _as_u32(r), _as_u32(cc), sv.contiguous()

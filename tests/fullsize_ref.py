@@ -187,3 +187,35 @@ def as_numpy_like(got: np.ndarray, want: torch.Tensor) -> np.ndarray:
     if got.dtype == np.float64:
         return w.astype(np.float64)
     return w.astype(np.int64)
+
+
+NAMES = {0: "crs", 1: "crs", 2: "crs", 3: "csb", 4: "csbh", 5: "bcoh", 6: "bcohc", 7: "bcohch", 8: "bcohchp",
+         9: "mergeb", 10: "mergebh"}
+
+
+def expected(sp, alg, m, n, r, c, v, lb, p):
+    """The storage arrays of engine `alg` (BCOH: p bands) recomputed from the documented keys."""
+    if alg <= 2:
+        return crs(m, r, c, v)
+    if alg in (3, 4):
+        return csb(m, n, r, c, v, lb, alg == 4)
+    if alg in (9, 10):
+        return mergeb(m, n, r, c, v, lb, alg == 10)
+    prefix = np.zeros(m + 1, dtype=np.uint64)
+    prefix[1:] = np.cumsum(torch.bincount(r.long(), minlength=m).cpu().numpy())
+    bounds = sp.partition_rows_by_nnz(prefix.astype(np.uint32), p, lb).tolist()
+    return bcoh(m, n, r, c, v, lb, bounds, NAMES[alg])
+
+
+def assert_format_bit_exact(sp, f, exp, what):
+    """Every storage_report array of built format f equals exp[name] bit for bit (on the device)."""
+    for a in sp.storage_report(f).arrays:
+        got = f.array_device(a.name)
+        want = exp[a.name]
+        assert got.numel() == want.numel(), (what, a.name, got.numel(), want.numel())
+        if got.dtype == torch.float64:
+            ok = torch.equal(got.view(torch.int64), want.to(torch.float64).contiguous().view(torch.int64))
+        else:
+            ok = torch.equal(got, want.to(torch.int64))
+        assert ok, f"{what}: {a.name} differs at full size"
+        del got, want

@@ -14,8 +14,6 @@ import fullsize_ref as fr
 
 pytestmark = pytest.mark.gpu
 
-NAMES = {0: "crs", 3: "csb", 4: "csbh", 5: "bcoh", 6: "bcohc", 7: "bcohch", 8: "bcohchp", 9: "mergeb",
-         10: "mergebh"}
 P = 8  # BCOH bands
 
 
@@ -26,32 +24,13 @@ def cfg2(cuda):
     return m, n, r, c, v
 
 
-def _expected(sp, alg, m, n, r, c, v, lb):
-    if alg <= 2:
-        return fr.crs(m, r, c, v)
-    if alg in (3, 4):
-        return fr.csb(m, n, r, c, v, lb, alg == 4)
-    if alg in (9, 10):
-        return fr.mergeb(m, n, r, c, v, lb, alg == 10)
-    prefix = np.zeros(m + 1, dtype=np.uint64)
-    prefix[1:] = np.cumsum(torch.bincount(r.long(), minlength=m).cpu().numpy())
-    bounds = sp.partition_rows_by_nnz(prefix.astype(np.uint32), P, lb).tolist()
-    return fr.bcoh(m, n, r, c, v, lb, bounds, NAMES[alg])
-
-
 @pytest.mark.parametrize("alg", [0, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_conversion_bit_exact_full_size(cuda, cfg2, alg):
     sp = cuda
     m, n, r, c, v = cfg2
     f = sp.build_format(alg, sp.TripletMatrix(m, n, r, c, v), P)
-    exp = _expected(sp, alg, m, n, r, c, v, f.info["log2_beta"])
-    for a in sp.storage_report(f).arrays:
-        got = f.array(a.name)
-        want = fr.as_numpy_like(got, exp[a.name])
-        assert got.shape == want.shape, (NAMES[alg], a.name, got.shape, want.shape)
-        cmp = got.astype(np.float64) if got.dtype == np.float64 else got.astype(np.int64)
-        assert np.array_equal(cmp, want), f"{NAMES[alg]}: {a.name} differs at full size"
-        del got, want, cmp
+    exp = fr.expected(sp, alg, m, n, r, c, v, f.info["log2_beta"], P)
+    fr.assert_format_bit_exact(sp, f, exp, fr.NAMES[alg])
     del f, exp
     torch.cuda.empty_cache()
 
@@ -102,3 +81,43 @@ def test_integer_exact_full_size(cuda, cfg2):
         y = sp.run_spmv(alg, f, ones, p=P)
         assert bool((y == y_ref).all()), sp.algorithm_name(alg)
         del f
+
+
+@pytest.mark.parametrize("alg", [2, 9])
+def test_cfg2_pinned_to_reference(cuda, reference, cfg2, alg):
+    """cfg2 pinned directly to the unmodified reference (oracle/_ref, the reference headers compiled
+    by oracle/Makefile) built on this box's host cores from the same COO: every storage array of
+    CRS (triplet_to_crs, inc/crs.hpp:67-91) and MergeB (build_mergeb, inc/mergeb.hpp:50-108) bit for
+    bit; for CRS also y -- merge against the reference's spmv_merge within 1e-12 * sum|a_ij x_j|,
+    SeqCrs bitwise against spmv_crs_seq."""
+    sp = cuda
+    m, n, r, c, v = cfg2
+    rows, cols, vals = r.cpu().numpy().view(np.uint32), c.cpu().numpy().view(np.uint32), v.cpu().numpy()
+    th = max(1, reference.hardware_threads())
+    ref = reference.build(alg, m, n, rows, cols, vals, threads=th, build_threads=th)
+    f = sp.build_format(alg, sp.TripletMatrix(m, n, r, c, v), th)
+    names = [a.name for a in sp.storage_report(f).arrays]
+    assert names == [nm for nm, _ in ref.storage]
+    for nm in names:
+        got, want = f.array(nm), ref.arrays[nm]
+        assert got.shape == want.shape, nm
+        if got.dtype == np.float64:
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), nm
+        else:
+            assert np.array_equal(got.astype(np.int64), want.astype(np.int64)), nm
+    if alg == 2:
+        x = np.random.default_rng(21).uniform(-1, 1, n)
+        xt = torch.from_numpy(x).cuda()
+        y = sp.run_spmv(2, f, xt, p=th).cpu().numpy()
+        y_ref = reference.spmv(ref, 2, x, p=th)
+        rp = f.array("row_ptr").astype(np.int64)
+        ri = torch.from_numpy(np.repeat(np.arange(m), np.diff(rp))).cuda()
+        prod = (torch.from_numpy(f.array("data")).cuda() *
+                xt[torch.from_numpy(f.array("col_ind").astype(np.int64)).cuda()]).abs()
+        bound = torch.zeros(m, dtype=torch.float64, device="cuda").index_add_(0, ri, prod).cpu().numpy()
+        assert np.all(np.abs(y - y_ref) <= 1e-12 * bound)
+        y0 = sp.run_spmv(0, sp.build_format(0, sp.TripletMatrix(m, n, r, c, v), 1), xt, p=1).cpu().numpy()
+        ref0 = reference.build(0, m, n, rows, cols, vals, threads=1, build_threads=th)
+        np.testing.assert_array_equal(y0, reference.spmv(ref0, 0, x, p=1))
+    del f
+    torch.cuda.empty_cache()

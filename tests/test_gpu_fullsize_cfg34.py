@@ -1,7 +1,9 @@
 """Full-size checks at BASELINE configs[2] (Zipf, n = 2^24, ~90 M nonzeros) and configs[3]
-(permuted 5-point Laplacian 4096^2, 84 M nonzeros), where the CPU oracle is too slow: size-
-independent properties on the device.
+(permuted 5-point Laplacian 4096^2, 84 M nonzeros), where the CPU oracle is too slow:
 
+* every conversion is BIT-EXACT: all storage arrays of all 11 engines equal the arrays recomputed
+  from the documented sort keys by the torch restatement (tests/fullsize_ref.py, pinned to the C
+  oracle in test_fullsize_ref_cpu.py), compared on the device;
 * every engine's y within 1e-12 * sum|a_ij x_j| of an fp64 scatter-add reference;
 * integer data with x = 1: every engine bitwise equal to the exact row sums;
 * linearity: A(x1 + 2 x2) == A x1 + 2 A x2 within the same normalised bound;
@@ -9,6 +11,8 @@ independent properties on the device.
   the CRS format decodes back to its coordinates (crs_to_icrs -> bicrs_to_triplet round trip)."""
 import pytest
 import torch
+
+import fullsize_ref as fr
 
 pytestmark = pytest.mark.gpu
 
@@ -22,7 +26,20 @@ def matrix(request, cuda):
     m, n, r, c, v = fn("cuda")
     yield name, m, n, r, c, v
     del r, c, v
-    torch.cuda.empty_cache()
+    cuda.release_cached_memory()
+
+
+@pytest.mark.parametrize("alg", [0, 3, 4, 5, 6, 7, 8, 9, 10])
+def test_conversion_bit_exact_full_size(cuda, matrix, alg):
+    sp = cuda
+    name, m, n, r, c, v = matrix
+    f = sp.build_format(alg, sp.TripletMatrix(m, n, r, c, v), P)
+    exp = fr.expected(sp, alg, m, n, r, c, v, f.info["log2_beta"], P)
+    try:
+        fr.assert_format_bit_exact(sp, f, exp, f"{name} {fr.NAMES[alg]}")
+    finally:
+        del f, exp
+        sp.release_cached_memory()
 
 
 def _ref(m, r, c, v, x):

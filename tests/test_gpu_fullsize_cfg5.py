@@ -1,8 +1,11 @@
 """Full-size checks at BASELINE configs[4] (R-MAT scale 26, column-normalised, ~1.06 G nonzeros:
-indices and offsets near the 32-bit limits, x of 537 MB): every engine's y within 1e-12 *
+indices and offsets near the 32-bit limits, x of 537 MB): the CRS conversion bit-exact against the
+torch restatement of its sort key (tests/fullsize_ref.py), every engine's y within 1e-12 *
 sum|a_ij x_j|, integer data bitwise, and two iterations of the application loop."""
 import pytest
 import torch
+
+import fullsize_ref as fr
 
 pytestmark = pytest.mark.gpu
 
@@ -12,9 +15,23 @@ def cfg5(cuda):
     from paper_2502_19284_b200 import gen
     name, fn = gen.CONFIGS[5]
     m, n, r, c, v = fn("cuda")
+    cuda.release_cached_memory()
     yield m, n, r, c, v
     del r, c, v
-    torch.cuda.empty_cache()
+    cuda.release_cached_memory()
+
+
+def test_crs_conversion_bit_exact_cfg5(cuda, cfg5):
+    sp = cuda
+    m, n, r, c, v = cfg5
+    f = sp.build_format(2, sp.TripletMatrix(m, n, r, c, v), 1)
+    sp.release_cached_memory()  # the build's sort scratch, before torch's own sorts below
+    exp = fr.crs(m, r, c, v)
+    try:
+        fr.assert_format_bit_exact(sp, f, exp, "cfg5 crs")
+    finally:
+        del f, exp
+        sp.release_cached_memory()
 
 
 def test_engines_full_size_cfg5(cuda, cfg5):
@@ -37,7 +54,7 @@ def test_engines_full_size_cfg5(cuda, cfg5):
             y2 = torch.zeros(m, dtype=torch.float64, device="cuda").index_add_(0, r.long(), v * y_ref[c.long()])
             assert bool(((xi - y2).abs() <= 1e-11 * y2.abs() + 1e-300).all())
         del f, y
-        torch.cuda.empty_cache()
+        sp.release_cached_memory()
 
 
 def test_integer_exact_cfg5(cuda, cfg5):
@@ -49,6 +66,7 @@ def test_integer_exact_cfg5(cuda, cfg5):
     a = sp.TripletMatrix(m, n, r, c, vi)
     for alg in (0, 2, 5, 8, 4):
         f = sp.build_format(alg, a, 8)
-        assert bool((sp.run_spmv(alg, f, ones, p=8) == want).all()), sp.algorithm_name(alg)
+        ok = bool((sp.run_spmv(alg, f, ones, p=8) == want).all())
         del f
-        torch.cuda.empty_cache()
+        sp.release_cached_memory()
+        assert ok, sp.algorithm_name(alg)
