@@ -86,14 +86,15 @@ __global__ void __launch_bounds__(256) blocked_spmv_kernel(
     const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc,
     const uint16_t* __restrict__ row_jump, const double* __restrict__ data,
     const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
-    const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc, uint32_t nchunks, unsigned lb,
-    const double* __restrict__ x, double* __restrict__ y) {
+    const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc, const uint32_t* __restrict__ ord,
+    uint32_t nchunks, unsigned lb, const double* __restrict__ x, double* __restrict__ y) {
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-  for (uint64_t c = gw; c < nchunks; c += nw) {
+  for (uint64_t q = gw; q < nchunks; q += nw) {
+    const uint32_t c = ord ? ord[q] : (uint32_t)q;  // column-panel schedule (x > L2) or storage order
     const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
     const uint2 rc = blk_rc[ch_blk[c]];
     const uint32_t rbase = rc.x << lb, cbase = rc.y << lb;
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   constexpr int U = 8;  // 8 x 32 = one full chunk in flight per warp
   for (uint32_t q = c0 + warp; q < c1; q += nwarps) {
-    const uint32_t c = ord ? ord[q] : q;  // chunks listed in block-row order (BCOH) or storage order
+    const uint32_t c = ord ? ord[q] : q;  // chunks in (panel, block row) order, or storage order
     const uint32_t e0 = ch_begin[c], e1 = ch_begin[c + 1];
     const uint32_t cbase = blk_rc[ch_blk[c]].y << lb;
     for (uint32_t base = e0; base < e1; base += 32 * U) {
@@ -283,7 +284,7 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
         f.find("packed")->as<uint32_t>(), f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
         f.find("chunk_blk")->as<uint32_t>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
         f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(),
-        f.find("win_chunk_order") ? f.find("win_chunk_order")->as<uint32_t>() : nullptr, f.log2_beta, f.m, x, y);
+        f.find("chunk_order") ? f.find("chunk_order")->as<uint32_t>() : nullptr, f.log2_beta, f.m, x, y);
     timing_end(s);
     return check_launch("spmv_blocked(window)");
   }
@@ -293,18 +294,20 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   const DevArray* ci = f.find("col_inc");
   const DevArray* rj = f.find("row_jump");
   const DevArray* cs = f.find("chunk_state");
+  const DevArray* co = f.find("chunk_order");
+  const uint32_t* ord = co ? co->as<uint32_t>() : nullptr;
   note_launch();
   timing_begin(icrs ? "blocked_spmv_kernel<icrs>" : "blocked_spmv_kernel<packed>", s);
   if (icrs)
     blocked_spmv_kernel<true><<<blocks, 256, 0, s>>>(
         nullptr, ci->as<uint16_t>(), rj->as<uint16_t>(), f.find("data")->as<double>(),
         f.find("chunk_begin")->as<uint32_t>(), f.find("chunk_blk")->as<uint32_t>(), cs->as<uint4>(),
-        f.find("blk_rc")->as<uint2>(), f.work_items, f.log2_beta, x, y);
+        f.find("blk_rc")->as<uint2>(), ord, f.work_items, f.log2_beta, x, y);
   else
     blocked_spmv_kernel<false><<<blocks, 256, 0, s>>>(
         pk->as<uint32_t>(), nullptr, nullptr, f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
-        f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), f.work_items, f.log2_beta, x,
-        y);
+        f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), ord, f.work_items, f.log2_beta,
+        x, y);
   timing_end(s);
   return check_launch("spmv_blocked");
 }

@@ -441,16 +441,23 @@ __device__ __forceinline__ uint32_t win_br(const uint32_t* ord, const uint32_t* 
                                            uint32_t q) {
   return blk_rc[ch_blk[ord ? ord[q] : q]].x;
 }
+__device__ __forceinline__ uint32_t win_panel(const uint32_t* ord, const uint32_t* ch_blk, const uint2* blk_rc,
+                                              uint32_t q, unsigned lb, uint32_t panels, uint32_t width) {
+  if (panels <= 1) return 0u;
+  return min(panels - 1, (uint32_t)(((uint64_t)blk_rc[ch_blk[ord ? ord[q] : q]].y << lb) / width));
+}
 
 // Window-item plan over the chunk sequence q -> chunk ord[q] (identity when ord is null): items
-// start at every block-row change and every kWinChunks-th position, so an item never crosses a
-// block row.
+// start at every (panel, block row) change and every per_item-th position, so an item never
+// crosses a block row or a panel.  head bit 1: an item starts; bit 2: a block row starts.
 __global__ void win_heads(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ ch_blk,
-                          const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t per_item,
-                          uint32_t* __restrict__ head) {
+                          const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t per_item, unsigned lb,
+                          uint32_t panels, uint32_t width, uint32_t* __restrict__ head) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nchunks) return;
-  const bool row_start = q == 0 || win_br(ord, ch_blk, blk_rc, q) != win_br(ord, ch_blk, blk_rc, q - 1);
+  const bool row_start = q == 0 || win_br(ord, ch_blk, blk_rc, q) != win_br(ord, ch_blk, blk_rc, q - 1) ||
+                         win_panel(ord, ch_blk, blk_rc, q, lb, panels, width) !=
+                             win_panel(ord, ch_blk, blk_rc, q - 1, lb, panels, width);
   head[q] = row_start ? 3u : (q % per_item == 0 ? 1u : 0u);
 }
 
@@ -459,10 +466,12 @@ __global__ void win_flag(const uint32_t* __restrict__ head, uint32_t nchunks, ui
   if (c < nchunks) flag[c] = head[c] != 0u;
 }
 
+// item_whole: the item covers its block row entirely (one panel, one item) -> stores its window.
 __global__ void win_fill(const uint32_t* __restrict__ head, const uint32_t* __restrict__ scan,
                          const uint32_t* __restrict__ ord, const uint32_t* __restrict__ ch_blk,
-                         const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t* __restrict__ item_chunk,
-                         uint32_t* __restrict__ item_br, uint32_t* __restrict__ item_whole) {
+                         const uint2* __restrict__ blk_rc, uint32_t nchunks, uint32_t panels,
+                         uint32_t* __restrict__ item_chunk, uint32_t* __restrict__ item_br,
+                         uint32_t* __restrict__ item_whole) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nchunks || !head[q]) return;
   const uint32_t i = scan[q];
@@ -470,14 +479,18 @@ __global__ void win_fill(const uint32_t* __restrict__ head, const uint32_t* __re
   while (e < nchunks && !head[e]) ++e;
   item_chunk[i] = q;
   item_br[i] = win_br(ord, ch_blk, blk_rc, q);
-  item_whole[i] = (head[q] & 2u) && (e == nchunks || (head[e] & 2u)) ? 1u : 0u;
+  item_whole[i] = panels <= 1 && (head[q] & 2u) && (e == nchunks || (head[e] & 2u)) ? 1u : 0u;
 }
 
-__global__ void win_order_keys(const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc,
-                               uint32_t nchunks, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Schedule key of a chunk: (column panel of its block, block row); panel = first column / width.
+__global__ void sched_keys(const uint32_t* __restrict__ ch_blk, const uint2* __restrict__ blk_rc,
+                           uint32_t nchunks, unsigned lb, uint32_t panels, uint32_t width, int brbits,
+                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
-  keys[c] = blk_rc[ch_blk[c]].x;
+  const uint2 rc = blk_rc[ch_blk[c]];
+  const uint32_t panel = panels > 1 ? min(panels - 1, (uint32_t)(((uint64_t)rc.y << lb) / width)) : 0u;
+  keys[c] = ((uint64_t)panel << brbits) | rc.x;
   vals[c] = c;
 }
 
@@ -597,35 +610,61 @@ static int blocked_common(BlockedBuild& bb, const spmvlab_cuda_coo& a, const uin
 // Chunks per window item: R-MAT s22 CSB 741 / 671 / 636 / 667 / 711 / 1226 us at 64 / 128 / 256 /
 // 512 / 1024 / 4096 (window zero + write-out per item vs. the tail of one 1024-thread CTA per SM).
 constexpr uint32_t kWinChunks = 256;
+// x bytes per column panel of the chunk schedule (see schedule_plan)
+constexpr uint64_t kBlkPanelXBytes = 48ull << 20;
 
-// `permute`: the block rows are not contiguous in storage (BCOH's Hilbert-ordered blocks), so the
-// chunks are first listed in block-row order ("win_chunk_order", a stable sort of chunk ids by
-// block row) and the items are runs of that list.
-static int window_plan(Format& f, Arena& ar, bool curve_in_block, bool permute = false) {
-  const char* env = std::getenv("SPMVLAB_BLOCKED_WINDOW");
-  const bool want = env && env[0] ? env[0] == '1' : curve_in_block;
-  if (!want || f.log2_beta > 14 || f.work_items == 0) return kOk;
+// The multiply's chunk schedule.
+//  * Column panels: when x outgrows the L2 (configs 3-5), every chunk walk in storage order sweeps
+//    all of x once per block row (cfg3 MergeB: 7.97 GB of DRAM reads for 1.35 GB of algorithmic
+//    bytes).  K = ceil(8n / kBlkPanelXBytes) panels of block columns are run one after the other
+//    ("chunk_order" = the chunk ids stably sorted by (panel, block row)), so one panel's x window
+//    stays L2-resident while its blocks stream past; y rows are then revisited once per panel.
+//    Measured (B200, panel MB 4096 / 96 / 64 / 48 / 32 / 24): cfg3 MergeB 1.86 / 1.56 / 1.56 /
+//    1.47 / 1.36 / 1.32 ms, BCOH 1.88 / 1.59 / 1.60 / 1.42 / 1.27 / 1.26; cfg4 MergeB 1.42 / 1.24 /
+//    1.23 / 1.15 / 1.54 / 1.33, BCOH 1.02 / 1.09 / 1.08 / 1.05 / 1.19 / 1.08.  What is left is one
+//    fp64 L2 reduction per element: the blocks are hypersparse at the reference's beta (cfg3 ~86
+//    nonzeros per 2^14 x 2^14 block), so runs of equal rows are ~1 long.
+//  * Window items (curve_in_block): runs of the same ordered list that never cross a (panel,
+//    block row) pair; an item owning a whole block row stores its window, the others add theirs.
+//    BCOH's Hilbert-ordered blocks interleave block rows (`permute`), so there the list is sorted
+//    even with one panel.
+static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute = false) {
+  if (f.work_items == 0) return kOk;
   cudaStream_t s = ar.stream();
+  const char* env = std::getenv("SPMVLAB_BLOCKED_WINDOW");
+  const bool window = (env && env[0] ? env[0] == '1' : curve_in_block) && f.log2_beta <= 14;
+  uint64_t xbytes = kBlkPanelXBytes;
+  if (const char* e = std::getenv("SPMVLAB_BLK_PANEL_MB")) xbytes = (uint64_t)std::max(1, atoi(e)) << 20;
+  const uint64_t want_panels = (8ull * f.n + xbytes - 1) / xbytes;
+  // (window formats keep one panel: their per-element shared-memory adds, not x, bound them, and
+  // the per-(panel, block row) window flushes cost more than the x locality saves -- cfg3 CSB
+  // 1.89 -> 2.01 ms with 48 MB panels)
+  f.blk_panels = window ? 1u : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want_panels, f.block_cols));
+  const uint32_t width = (uint32_t)(((uint64_t)f.n + f.blk_panels - 1) / f.blk_panels);
   const uint32_t nch = (uint32_t)f.work_items;
   const uint32_t* ch_blk = f.find("chunk_blk")->as<uint32_t>();
   const uint2* blk_rc = f.find("blk_rc")->as<uint2>();
-  uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
-  uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
-  if (!head || !flag) return kNoMemory;
   const uint32_t* ord = nullptr;
-  if (permute) {
+  if (f.blk_panels > 1 || (window && permute)) {
+    const int brbits = std::max(1, (int)bit_width64(f.block_rows ? f.block_rows - 1 : 0));
+    const int pbits = (int)bit_width64(f.blk_panels - 1);
     uint64_t* k1 = ar.alloc_n<uint64_t>(nch);
     uint64_t* k2 = ar.alloc_n<uint64_t>(nch);
     uint32_t* v2 = ar.alloc_n<uint32_t>(nch);
-    uint32_t* v1 = static_cast<uint32_t*>(f.add("win_chunk_order", nch, 4, s));
+    uint32_t* v1 = static_cast<uint32_t*>(f.add("chunk_order", nch, 4, s));
     if (!k1 || !k2 || !v1 || !v2) return kNoMemory;
-    win_order_keys<<<(nch + 255) / 256, 256, 0, s>>>(ch_blk, blk_rc, nch, k1, v1);
-    const int brbits = std::max(1, (int)bit_width64(f.block_rows ? f.block_rows - 1 : 0));
-    if (radix_sort_pairs(k1, k2, v1, v2, nch, 0, brbits, ar))
+    sched_keys<<<(nch + 255) / 256, 256, 0, s>>>(ch_blk, blk_rc, nch, f.log2_beta, f.blk_panels, width, brbits,
+                                                   k1, v1);
+    if (radix_sort_pairs(k1, k2, v1, v2, nch, 0, brbits + pbits, ar))
       cudaMemcpyAsync(v1, v2, 4ull * nch, cudaMemcpyDeviceToDevice, s);
     ord = v1;
   }
-  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, kWinChunks, head);
+  if (!window) return check_launch("schedule_plan");
+  uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
+  uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
+  if (!head || !flag) return kNoMemory;
+  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, kWinChunks, f.log2_beta, f.blk_panels,
+                                               width, head);
   win_flag<<<(nch + 255) / 256, 256, 0, s>>>(head, nch, flag);  // flag = head != 0
   exclusive_scan_u32(flag, flag, nch, ar);                        // -> item index of each head
   uint32_t nitems = 0;
@@ -635,9 +674,9 @@ static int window_plan(Format& f, Arena& ar, bool curve_in_block, bool permute =
   uint32_t* item_whole = static_cast<uint32_t*>(f.add("win_item_whole", nitems, 4, s));
   if (!item_chunk || !item_br || !item_whole) return kNoMemory;
   cudaMemcpyAsync(item_chunk + nitems, &nch, 4, cudaMemcpyHostToDevice, s);
-  win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ord, ch_blk, blk_rc, nch, item_chunk, item_br,
-                                              item_whole);
-  return check_launch("window_plan");
+  win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ord, ch_blk, blk_rc, nch, f.blk_panels, item_chunk,
+                                              item_br, item_whole);
+  return check_launch("schedule_plan");
 }
 
 static Geom base_geom(const Format& f, unsigned lb) {
@@ -678,7 +717,7 @@ int build_csb(Format& f, const spmvlab_cuda_coo& a, unsigned lb, bool hilbert, u
     return d.name == "blk_ptr" || d.name == "packed" || d.name == "data";
   });
   f.nstorage = 3;
-  if (int rc = window_plan(f, ar, true)) return rc;
+  if (int rc = schedule_plan(f, ar, true)) return rc;
   return check_launch("build_csb");
 }
 
@@ -724,7 +763,7 @@ int build_mergeb(Format& f, const spmvlab_cuda_coo& a, unsigned lb, bool hilbert
   }
   f.arrays = sorted;
   f.nstorage = 5;
-  if (int rc = window_plan(f, ar, hilbert)) return rc;
+  if (int rc = schedule_plan(f, ar, hilbert)) return rc;
   return check_launch("build_mergeb");
 }
 
@@ -977,9 +1016,10 @@ int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned lb, unsigned p, Ar
   }
   f.arrays = sorted;
   f.nstorage = 8;
-  // Hilbert in-block (packed) variants: block-row windows over a block-row ordering of the chunks
-  if (a.nnz && helem)
-    if (int rc = window_plan(f, ar, true, true)) return rc;
+  // chunk schedule: column panels when x outgrows the L2; the Hilbert in-block (packed) variants
+  // get block-row windows over a block-row ordering of the chunks
+  if (a.nnz)
+    if (int rc = schedule_plan(f, ar, helem, helem)) return rc;
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_bcoh");
   return check_launch("build_bcoh");
 }

@@ -51,6 +51,9 @@ struct spmvlab_cuda_format {
   // ---- blocked plan (CSB / MergeB / BCOH): work items = (element range, y window)
   uint32_t work_items = 0;
   bool needs_zero_y = false;
+  // column panels of the chunk schedule (x larger than the L2): chunks run panel by panel
+  // ("chunk_order" / the window items), so one panel's x window stays L2-resident
+  uint32_t blk_panels = 1;
 
   // ---- per-stream multiply scratch (merge carries), so one immutable format can serve
   // concurrent multiplies on different streams / host threads (inc/engine.hpp ownership rules).
