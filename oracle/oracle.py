@@ -335,6 +335,12 @@ def _cache_read(fn, free, path):
     return out
 
 
+class RefBenchRecord(C.Structure):
+    _fields_ = [("alg", C.c_int), ("threads", C.c_uint), ("min_time", C.c_double), ("speedup", C.c_double),
+                ("convert_time", C.c_double), ("convert_ratio", C.c_double), ("density", C.c_double),
+                ("status", C.c_char * 128)]
+
+
 class Reference:
     """The unmodified reference (oracle/_ref/libspmvref.so)."""
 
@@ -381,6 +387,11 @@ class Reference:
                                      C.POINTER(C.c_void_p)]
         L.ref_to_triplet.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_double)]
+        L.ref_bench.restype = C.c_int64
+        L.ref_bench.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_uint,
+                                C.POINTER(C.c_uint), C.c_uint, C.c_uint, C.c_uint, C.c_uint,
+                                C.POINTER(RefBenchRecord), C.c_uint64]
         L.ref_csb_leaves.restype = C.c_int64
         L.ref_csb_leaves.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64]
 
@@ -451,6 +462,28 @@ class Reference:
 
     def storage_total(self, built: Built) -> int:
         return int(self.lib.ref_storage_total(built.handle.h))
+
+    def bench(self, kind: int, m: int, n: int, rows, cols, vals, algs, threads, spmv_reps: int = 550,
+              convert_reps: int = 25, warmup: int = 5) -> list:
+        """The reference's bench_spmv (kind 0) / bench_convert (kind 1), inc/bench.hpp:239-329, run
+        unmodified on this host: one dict per (algorithm, threads)."""
+        rows, cols, vals = _coo_args(rows, cols, vals)
+        a = (C.c_int * len(algs))(*algs)
+        t = (C.c_uint * len(threads))(*threads)
+        cap = len(algs) * len(threads)
+        out = (RefBenchRecord * cap)()
+        k = self.lib.ref_bench(kind, m, n, len(vals), _p(rows, C.c_uint32), _p(cols, C.c_uint32),
+                               _p(vals, C.c_double), a, len(algs), t, len(threads), spmv_reps, convert_reps,
+                               warmup, out, cap)
+        if k < 0:
+            raise CheckerError(int(-k), f"ref_bench: {self.lib.ref_last_error().decode()}")
+        recs = []
+        for r in out[:k]:
+            recs.append({"alg": r.alg, "threads": r.threads, "min_time_s": r.min_time, "speedup": r.speedup,
+                         "convert_time_s": None if r.convert_time < 0 else r.convert_time,
+                         "convert_ratio": None if r.convert_ratio < 0 else r.convert_ratio,
+                         "density": r.density, "status": r.status.decode()})
+        return recs
 
     def to_triplet(self, built: Built):
         """crs_/csb_/mergeb_/bcoh_to_triplet: (rows, cols, vals) in the reference's order."""

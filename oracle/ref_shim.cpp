@@ -343,4 +343,50 @@ int64_t ref_csb_leaves(void* hv, uint64_t threshold, uint64_t* out, uint64_t cap
   return static_cast<int64_t>(k);
 }
 
+// The reference's own measurement protocol (inc/bench.hpp:239-329), unmodified: kind 0 =
+// bench_spmv (build per (algorithm, threads), verify against spmv_triplet, min of spmv_reps
+// multiplies; speedup over the sequential CRS baseline), kind 1 = bench_convert (min of
+// convert_reps conversions; ratio to the fastest ParCRS multiply).  One record per (alg, p).
+struct ref_bench_record {
+  int alg;
+  unsigned threads;
+  double min_time, speedup, convert_time, convert_ratio, density;
+  char status[128];
+};
+
+int64_t ref_bench(int kind, uint32_t m, uint32_t n, uint64_t nnz, const uint32_t* rows, const uint32_t* cols,
+                  const double* vals, const int* algs, unsigned nalgs, const unsigned* threads, unsigned nthreads,
+                  unsigned spmv_reps, unsigned convert_reps, unsigned warmup, ref_bench_record* out,
+                  uint64_t capacity) {
+  try {
+    auto a = make_triplet(m, n, nnz, rows, cols, vals);
+    BenchConfig cfg;
+    cfg.algorithms.clear();
+    for (unsigned i = 0; i < nalgs; ++i) cfg.algorithms.push_back(static_cast<Algorithm>(algs[i]));
+    cfg.threads.assign(threads, threads + nthreads);
+    cfg.spmv_reps = spmv_reps;
+    cfg.convert_reps = convert_reps;
+    cfg.warmup = warmup;
+    const auto recs = kind == 0 ? bench_spmv(a, "m", cfg) : bench_convert(a, "m", cfg);
+    uint64_t k = 0;
+    for (const auto& r : recs) {
+      if (k >= capacity) return -2;
+      ref_bench_record& o = out[k++];
+      o.alg = static_cast<int>(r.algorithm);
+      o.threads = r.threads;
+      o.min_time = r.min_time;
+      o.speedup = r.speedup;
+      o.convert_time = r.convert_time ? *r.convert_time : -1.0;
+      o.convert_ratio = r.convert_ratio ? *r.convert_ratio : -1.0;
+      o.density = r.density;
+      std::memset(o.status, 0, sizeof(o.status));
+      std::strncpy(o.status, r.status.c_str(), sizeof(o.status) - 1);
+    }
+    return static_cast<int64_t>(k);
+  } catch (const Error& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 }  // extern "C"
