@@ -8,12 +8,16 @@ merge-CSR multiply y = A x (the north-star engine, spmv_merge) through the C ABI
 resident in HBM; `value` = 2 nnz K / t  (GFLOP/s).  Inputs (866 MB of algorithmic bytes) are
 larger than the 126 MB L2, so no flush is needed between steps.
 
-N > 1 (torchrun, one process per GPU): the same matrix is row-sharded by nonzeros across ranks
-(partition_rows_by_nnz with beta = 1, inc/block_size.hpp:73-102); a step is x_next = A x on every
-rank: the local multiply whose epilogue stores each finished row into every rank's next x (CUDA
-IPC peer stores; --exchange nccl: the local multiply followed by an NCCL all-gatherv of the y_r
-slices), then a stream-ordered rendezvous; time is the max over ranks; scaling "strong";
-"multi_gpu" reports the shard multiply alone beside the step (compute vs exchange).
+N > 1 (torchrun, one process per GPU): BASELINE configs[4] by default -- R-MAT scale 26, column-
+normalised, the iterated x <- A x of north_star's multi-GPU row (--config overrides).  The matrix
+is row-sharded by nonzeros across ranks (partition_rows_by_nnz with beta = 1,
+inc/block_size.hpp:73-102); a step is one iteration x_next = A x on every rank: the local multiply
+whose warp tiles copy their finished rows into every rank's next x (CUDA IPC peer stores over
+NVLink, --exchange fused, default) or the local multiply followed by an NCCL all-gatherv of the y_r
+slices (--exchange nccl), then a stream-ordered rendezvous; time is the max over ranks; scaling
+"strong".  "multi_gpu" reports, on the same matrix: the 1-GPU step (rank 0 multiplies the whole
+matrix before sharding), the shard multiply alone, and step / exchange time of BOTH exchanges
+(SURVEY §8e).
 
 Extra keys: e2e (host buffers through the C ABI, copies timed), roofline (dominant kernel,
 event-timed in the library), cpu_baseline (the reference's own engine on the host cores),
@@ -268,7 +272,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config (default: 2 on 1 GPU, 5 -- the iterated scale-26 matrix -- on N > 1)")
     ap.add_argument("--no-formats", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
@@ -279,6 +284,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = 2 if world == 1 else 5
     # SPMVLAB_BENCH_BACKEND=gloo (test only): N ranks as processes sharing fewer GPUs, synchronised
     # on the host (no kernel waits on another rank), to exercise the N > 1 flow on a 1-GPU box.
     backend = os.environ.get("SPMVLAB_BENCH_BACKEND", "nccl")
@@ -309,6 +316,22 @@ def main():
     name, m, n, r, c, v = make_matrix(args.config, dev)
     nnz_total = v.numel()
     from paper_2502_19284_b200 import dist as sdist
+    x = torch.rand(n, generator=torch.Generator(device=dev).manual_seed(7), device=dev, dtype=torch.float64)
+
+    # N > 1: the same matrix on ONE GPU first (rank 0, before sharding), so the 1 -> N curve in
+    # the line is on one matrix
+    single_gpu = None
+    if world > 1 and rank == 0 and m == n:
+        f1 = sp.build_format(sp.Algorithm.Merge, sp.TripletMatrix(m, n, r, c, v), 1)
+        y1 = torch.empty(m, dtype=torch.float64, device=dev)
+        reps1 = max(3, min(args.steps, 20))
+        ts = ev_time(lambda: sp.run_spmv(sp.Algorithm.Merge, f1, x, y1, p=1), reps1, 3, stream)
+        ms1 = statistics.median(ts)
+        single_gpu = {"ms_per_step": ms1, "gflops": 2.0 * nnz_total / (ms1 / 1e3) / 1e9, "steps": reps1,
+                      "merge_panels": f1.info["merge_panels"]}
+        del f1, y1
+        sp.release_cached_memory()
+
     cuts = [0, m]
     if world > 1:
         cuts = sdist.shard_bounds(sdist.row_prefix(m, r), world)
@@ -317,7 +340,6 @@ def main():
     else:
         a = sp.TripletMatrix(m, n, r, c, v)
     m_loc = a.m
-    x = torch.rand(n, generator=torch.Generator(device=dev).manual_seed(7), device=dev, dtype=torch.float64)
 
     # conversion (COO -> merge-CSR), event-timed, min of 2 (the first also warms the memory pools)
     conv_ms = float("inf")
@@ -329,49 +351,71 @@ def main():
         e1.record(stream)
         e1.synchronize()
         conv_ms = min(conv_ms, e0.elapsed_time(e1))
+    if world > 1:
+        del lr, lc, lv
+        sp.release_cached_memory()
     y_full = torch.zeros(m, dtype=torch.float64, device=dev)
     y_loc = y_full[cuts[rank]:cuts[rank + 1]] if world > 1 else y_full
 
     sharded = sdist.ShardedSpMV(cuts, rank, lambda xf, yl: sp.run_spmv(sp.Algorithm.Merge, fmt, xf, yl, p=1))
-    fused, exchange = None, "none (1 GPU)"
+    fused, fused_err = None, None
     if world > 1:
-        exchange = "NCCL all-gatherv (per-rank broadcasts) of the y slices"
-        if args.exchange == "fused":
-            try:  # collective; every rank agrees on success or falls back together
-                fused = sdist.FusedExchangeSpMV(cuts, rank, fmt, n)
-                fused.load(x)
-                exchange = "fused: merge-kernel epilogue stores rows into every rank's next x (CUDA IPC, NVLink)"
-            except Exception as ex:
-                log(f"fused exchange unavailable, using NCCL: {ex}")
-                fused = None
-                exchange += f" (fused unavailable: {ex})"
+        try:  # collective; every rank agrees on success or falls back together
+            fused = sdist.FusedExchangeSpMV(cuts, rank, fmt, n)
+            fused.load(x)
+        except Exception as ex:
+            log(f"fused exchange unavailable: {ex}")
+            fused, fused_err = None, str(ex)
+    EXCH = {"fused": "fused: each merge warp tile copies its finished rows into every rank's next x (CUDA IPC "
+                     "peer stores over NVLink)",
+            "nccl": "NCCL all-gatherv (per-rank broadcasts) of the y slices"}
 
-    def step():
-        if fused is not None:
-            fused.step()  # x_next = A_r x on every rank: multiply + peer stores + rank barrier
-        elif world > 1:
-            sharded.step(x, y_full)  # local merge-CSR multiply + NCCL all-gatherv of the y slices
-        else:
-            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
+    def make_step(mode):
+        if mode == "fused":
+            return fused.step  # x_next = A_r x on every rank: multiply + peer stores + rank rendezvous
+        if mode == "nccl":
+            return lambda: sharded.step(x, y_full)  # local merge multiply + NCCL all-gatherv
+        return lambda: sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_loc, p=1)
 
+    def timed(fn, steps):
+        """Device time of `steps` calls (max over ranks), after a barrier."""
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            fn()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt[0])
+        return ms
+
+    modes = ["local"] if world == 1 else (["fused", "nccl"] if fused is not None else ["nccl"])
+    if world > 1 and args.exchange == "nccl":
+        modes = ["nccl"] + [md for md in modes if md != "nccl"]
+    primary = modes[0]
+    exchange = "none (1 GPU)" if world == 1 else EXCH[primary] + (f" (fused unavailable: {fused_err})" if fused_err else "")
+    step = make_step(primary)
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
     clocks = Clocks(local)
     clocks.start()
     launches0 = L.spmvlab_cuda_launch_count()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
-        step()
-    t1.record(stream)
-    torch.cuda.synchronize()
+    elapsed_ms = timed(step, args.steps)
     launches = L.spmvlab_cuda_launch_count() - launches0
     clk = clocks.stop()
+    if world > 1:
+        import torch.distributed as dist
+        tl = torch.tensor([float(launches)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        launches = int(tl[0])
     # dominant-kernel duration: a separate run with the library's per-launch event brackets (kept
     # out of the timed region above, where the extra event records would cost small kernels)
     L.spmvlab_cuda_kernel_timing(1)
@@ -382,55 +426,55 @@ def main():
     import ctypes as C
     kms, kl, kname = C.c_double(), C.c_uint64(), C.create_string_buffer(64)
     L.spmvlab_cuda_kernel_time(C.byref(kms), C.byref(kl), kname, 64)
-    elapsed_ms = t0.elapsed_time(t1)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([elapsed_ms, float(launches)], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed_ms, launches = float(mx[0]), int(sm[1])
     ms_step = elapsed_ms / args.steps
     value = 2.0 * nnz_total * args.steps / (elapsed_ms / 1e3) / 1e9
 
-    # N > 1: per-step compute (the shard's multiply alone, no exchange) beside the
-    # whole step, max over ranks; exchange = the difference
+    # N > 1: per-iteration compute (the shard's multiply alone, no exchange, max over
+    # ranks) and, for BOTH exchanges, the whole step and exchange = step - compute; plus the
+    # 1-GPU step on the same matrix
     multi_gpu = None
     if world > 1:
-        import torch.distributed as dist
-        y_only = torch.empty(m_loc, dtype=torch.float64, device=dev)
+        comp_fn = make_step("local")
         for _ in range(3):
-            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_only, p=1)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0.record(stream)
-        for _ in range(args.steps):
-            sp.run_spmv(sp.Algorithm.Merge, fmt, x, y_only, p=1)
-        t1.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        comp = float(tt[0]) / args.steps
-        multi_gpu = {"compute_ms_per_step": comp, "exchange_ms_per_step": max(0.0, ms_step - comp),
-                     "note": "compute = the rank's shard multiply alone (max over ranks); exchange = step - compute"}
-        del y_only
+            comp_fn()
+        comp = timed(comp_fn, args.steps) / args.steps
+        per = {}
+        for md in modes:
+            fn = make_step(md)
+            for _ in range(3):
+                fn()
+            st = timed(fn, args.steps) / args.steps
+            per[md] = {"step_ms": st, "exchange_ms": max(0.0, st - comp), "exchange": EXCH[md],
+                       "gflops": 2.0 * nnz_total / (st / 1e3) / 1e9}
+        multi_gpu = {"compute_ms_per_step": comp, "exchanges": per, "single_gpu": single_gpu,
+                     "cuts": cuts, "note": "compute = the rank's shard multiply alone (max over ranks); "
+                                           "exchange = step - compute; single_gpu = rank 0, whole matrix"}
+        if single_gpu:
+            multi_gpu["speedup_vs_1gpu"] = single_gpu["ms_per_step"] / ms_step
 
-    # dominant kernel roofline (per launch, this rank)
+    # dominant kernel roofline (per launch, this rank).  Algorithmic bytes of the timed kernels: the
+    # reference format (storage_report) + x once + y once; with K > 1 column panels the kernels read
+    # the panel arrays instead (row pointer K m + 1 entries, the same col / data) and y is written
+    # K times and read back K - 1 times, so those are the bytes counted.
     rep = sp.storage_report(fmt)
-    alg_bytes = rep.total() + 8 * n + 8 * m_loc
+    ref_bytes = rep.total() + 8 * n + 8 * m_loc
+    K = int(fmt.info["merge_panels"])
+    nnz_loc = fmt.nnz()
+    alg_bytes = ref_bytes if K == 1 else (4 * (K * m_loc + 1) + 12 * nnz_loc + 8 * n + (2 * K - 1) * 8 * m_loc)
     k_ms = kms.value / max(1, kl.value)
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     kernel_name = kname.value.decode()
-    roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": k_ms,
-                "algorithmic_bytes_per_launch": alg_bytes, "traffic": ncu_traffic(args.config, kernel_name),
+    roofline = {"bound": "hbm", "kernel": kernel_name + " + merge_fixup_kernel", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": k_ms,
+                "algorithmic_bytes_per_launch": alg_bytes, "reference_format_bytes": ref_bytes,
+                "column_panels": K, "traffic": ncu_traffic(args.config, kernel_name),
                 "share_of_step": k_ms / ms_step, "l2_sectors": l2_roofline(args.config, kernel_name, k_ms)}
 
     # End to end through the C ABI with host buffers: every step copies its own x in (pinned H2D),
     # multiplies, and copies its own y out (D2H).  Steps rotate over three streams with their own
     # staging buffers, so the H2D of later steps overlaps the multiply and D2H of earlier ones
     # (full-duplex PCIe) without waiting behind a stream's own D2H.
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     NS = 3
     e2e_streams = [torch.cuda.Stream(dev) for _ in range(NS)]
     x_host = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(NS)]

@@ -106,9 +106,11 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
  * own, its caller repeats inc/engine.hpp:126-148).  x (device, n) holds x_0 on entry and x_iters on
  * return; work is a device buffer of n doubles.  With SPMVLAB_ITER_NORMALIZE each iterate is
  * rescaled to unit L1 mass.  If `norms` (device, 2 * iters doubles) is non-NULL, iteration k writes
- * norms[2k] = ||x_{k+1} - x_k||_1 and norms[2k+1] = sum_i (A x_k)_i, the mass before any rescale
- * (its drop from the previous mass is the leakage through empty columns), both by deterministic
- * fixed-order reductions.  SPMVLAB_ITER_GRAPH captures one iteration pair (x -> work -> x) as a
+ * norms[2k] = ||A x_k - x_k||_1 (the residual; = ||x_{k+1} - x_k||_1 without rescaling) and
+ * norms[2k+1] = sum_i (A x_k)_i, the mass before any rescale (its drop from the previous mass is the
+ * leakage through empty columns), both by deterministic fixed-order reductions.  For the merge
+ * engine (2) the norms and the rescale are fused into the multiply (no extra pass over the
+ * vectors; the rescale is applied lazily by the next multiply).  SPMVLAB_ITER_GRAPH captures one iteration pair (x -> work -> x) as a
  * CUDA graph and replays it iters / 2 times (requires a non-default stream). */
 #define SPMVLAB_ITER_NORMALIZE 1
 #define SPMVLAB_ITER_GRAPH 2
@@ -125,14 +127,16 @@ int spmvlab_cuda_exchange_alloc(uint64_t bytes, void** dev_ptr, unsigned char ip
 int spmvlab_cuda_exchange_open(const unsigned char ipc_handle[64], void** dev_ptr);
 int spmvlab_cuda_exchange_close(void* dev_ptr, int opened);
 
-/* Merge-CSR multiply (algorithm 2) of a row shard whose epilogue also stores every finished row
- * r of y into dest[i][row_offset + r] for i < ndest (<= 8; device pointers valid in this process,
- * e.g. the peers' next-x buffers opened above): the all-gather of the y slices fused into the
- * multiply.  y (length m) is written as by run_spmv.  Synchronise the ranks before reading the
- * destinations. */
+/* Merge-CSR multiply (algorithm 2) of a row shard that also stores every finished row r of y into
+ * dest[i][row_offset + r] for i < ndest (<= 8; device pointers valid in this process, e.g. the
+ * peers' next-x buffers opened above, each dest_len doubles long): the all-gather of the y slices
+ * fused into the multiply -- each warp tile copies its finished rows to the peers as one
+ * contiguous run when it ends, the carry fix-up the rows it completes.  y (length m) is written as
+ * by run_spmv.  InvalidArgument if row_offset + m > dest_len.  Synchronise the ranks before
+ * reading the destinations. */
 int spmvlab_cuda_run_spmv_scatter(const spmvlab_cuda_format* f, const double* x, uint64_t x_len, double* y,
-                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t row_offset,
-                                  void* stream);
+                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t dest_len,
+                                  uint64_t row_offset, void* stream);
 
 /* storage_report(const BuiltFormat&) -- inc/engine.hpp:158-160 / inc/storage.hpp:62-123. */
 int spmvlab_cuda_storage_report(const spmvlab_cuda_format* f, spmvlab_cuda_storage_array* rows,

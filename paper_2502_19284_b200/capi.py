@@ -106,7 +106,7 @@ def load() -> C.CDLL:
     L.spmvlab_cuda_exchange_alloc.argtypes = [u64, C.POINTER(vp), C.POINTER(C.c_ubyte)]
     L.spmvlab_cuda_exchange_open.argtypes = [C.POINTER(C.c_ubyte), C.POINTER(vp)]
     L.spmvlab_cuda_exchange_close.argtypes = [vp, i]
-    L.spmvlab_cuda_run_spmv_scatter.argtypes = [vp, vp, u64, vp, u64, C.POINTER(vp), C.c_uint, u64, vp]
+    L.spmvlab_cuda_run_spmv_scatter.argtypes = [vp, vp, u64, vp, u64, C.POINTER(vp), C.c_uint, u64, u64, vp]
     L.spmvlab_cuda_run_spmv_host.argtypes = [i, vp, vp, u64, vp, u64, C.c_uint, C.POINTER(Options), vp, vp, vp]
     L.spmvlab_cuda_storage_report.argtypes = [vp, C.POINTER(StorageArray), C.c_size_t, C.POINTER(C.c_size_t)]
     L.spmvlab_cuda_get_format_info.argtypes = [vp, C.POINTER(FormatInfo)]

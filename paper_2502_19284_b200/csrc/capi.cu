@@ -352,13 +352,14 @@ int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, doubl
   auto mult = [&](const double* xi, double* yi, cudaStream_t st) {
     return spmvlab_cuda_run_spmv(alg, f, xi, f->n, yi, f->m, p, nullptr, st);
   };
-  if (!(flags & SPMVLAB_ITER_GRAPH) || iters == 0) return iterate(*f, mult, x, work, iters, flags, norms, s);
+  const bool fused = alg == kMerge && is_crs_alg(f->alg) && !std::getenv("SPMVLAB_ITER_UNFUSED");
+  if (!(flags & SPMVLAB_ITER_GRAPH) || iters == 0) return iterate(*f, mult, x, work, iters, flags, norms, s, fused);
   if (!s) return fail(kInvalidArgument, "graph mode needs a non-default stream");
   // nothing may allocate synchronously inside the capture: create this stream's carry scratch now
   if (alg == kMerge && is_crs_alg(f->alg) && !f->stream_scratch(s))
     return fail(kNoMemory, "device allocation failed (merge carry scratch)");
   const bool timing = timing_enable(false);  // no event brackets inside a capture
-  const int rc = iterate(*f, mult, x, work, iters, flags, norms, s);
+  const int rc = iterate(*f, mult, x, work, iters, flags, norms, s, fused);
   timing_enable(timing);
   return rc;
 }
@@ -400,12 +401,14 @@ int spmvlab_cuda_exchange_close(void* dev_ptr, int opened) {
 }
 
 int spmvlab_cuda_run_spmv_scatter(const spmvlab_cuda_format* f, const double* x, uint64_t x_len, double* y,
-                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t row_offset,
-                                  void* stream) {
+                                  uint64_t y_len, double* const* dest, unsigned ndest, uint64_t dest_len,
+                                  uint64_t row_offset, void* stream) {
   if (!f) return fail(kInvalidArgument, "null format");
   if (!is_crs_alg(f->alg)) return fail(kInvalidArgument, "format is not CRS");
   if (x_len != f->n || y_len != f->m) return fail(kDimensionMismatch, "x / y length does not match the matrix");
   if (ndest > kMaxRowDest || (ndest && !dest)) return fail(kInvalidArgument, "bad destination list");
+  if (ndest && row_offset + f->m > dest_len)
+    return fail(kInvalidArgument, "row_offset + m exceeds the destination buffers");
   RowDest d{};
   for (unsigned i = 0; i < ndest; ++i) d.p[i] = dest[i];
   d.n = ndest;

@@ -113,6 +113,13 @@ class FusedExchangeSpMV:
         self.rank, self.world = rank, len(cuts) - 1
         self.lo, self.hi = self.cuts[rank], self.cuts[rank + 1]
         self.fmt, self.n = fmt, n
+        # the shards must tile a square matrix: every rank's rows land in every peer's n-long
+        # buffer at their row offset (checked again by the library per multiply)
+        shape_err = None
+        if self.cuts[0] != 0 or self.cuts[-1] != n or any(a > b for a, b in zip(self.cuts, self.cuts[1:])):
+            shape_err = f"row cuts {self.cuts[0]}..{self.cuts[-1]} do not tile the n = {n} exchange buffers"
+        elif fmt.m != self.hi - self.lo or fmt.n != n:
+            shape_err = f"shard format is {fmt.m} x {fmt.n}, expected {self.hi - self.lo} x {n}"
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.group = group
         self.barrier = barrier or (lambda: dist.barrier(group))
@@ -121,8 +128,10 @@ class FusedExchangeSpMV:
         # stores are performed at kernel completion), and the host never waits.
         self._stream_barrier = barrier is None and dist.get_backend(group) == "nccl"
         self._token = torch.zeros(1, dtype=torch.float64, device=self.device)
-        self.own, handles, err = [], [], None
+        self.own, handles, err = [], [], shape_err
         try:
+            if err is not None:
+                raise ValueError(err)
             for _ in range(2):
                 p, h = C.c_void_p(), (C.c_ubyte * 64)()
                 _check(L.spmvlab_cuda_exchange_alloc(8 * max(n, 1), C.byref(p), h))
@@ -181,7 +190,7 @@ class FusedExchangeSpMV:
         y_local = self.ptr[nxt][self.rank] + 8 * self.lo  # own rows go straight into the own next x
         self._check(self.capi.load().spmvlab_cuda_run_spmv_scatter(
             self.fmt.handle, self.ptr[self.cur][self.rank], self.n, y_local, self.hi - self.lo, dest, len(peers),
-            self.lo, st.cuda_stream))
+            self.n, self.lo, st.cuda_stream))
         if self._stream_barrier:
             import torch.distributed as dist
             with torch.cuda.stream(st):

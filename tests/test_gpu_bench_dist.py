@@ -38,4 +38,9 @@ def test_bench_two_ranks(cuda, exchange):
     assert d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
     assert d["config"]["exchange"].startswith("fused" if exchange == "fused" else "NCCL")
     mg = d["multi_gpu"]
-    assert mg["compute_ms_per_step"] > 0 and mg["exchange_ms_per_step"] >= 0
+    assert mg["compute_ms_per_step"] > 0
+    assert set(mg["exchanges"]) == {"fused", "nccl"}  # both exchanges measured on the same shards
+    for e in mg["exchanges"].values():
+        assert e["step_ms"] > 0 and e["exchange_ms"] >= 0
+    assert mg["single_gpu"]["ms_per_step"] > 0 and mg["speedup_vs_1gpu"] > 0
+    assert len(mg["cuts"]) == 3

@@ -16,3 +16,15 @@ def test_cpp_dropin_parity(cuda):
         subprocess.run(["make", "-s", "-C", os.path.dirname(exe)], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_cpp_dropin_with_reference_types(cuda):
+    """tests/cpp/ref_types_dropin.cpp: the drop-in driven by spmvlab::TripletMatrix / DenseVector and
+    the acceptance criterion of /root/reference/proj/tests/acceptance.cpp:113-153, compiled here
+    against the unmodified reference headers (the prebuilt binary travels; the reference tree does
+    not exist on the GPU box)."""
+    exe = os.path.join(ROOT, "tests", "cpp", "ref_types_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("ref_types_dropin not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and " 0 failures" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]

@@ -112,8 +112,12 @@ def test_scatter_single_rank_equals_run_spmv(cuda, monkeypatch, panels):
     y = torch.empty(m, dtype=torch.float64, device="cuda")
     d1 = torch.full((m + 5,), -1.0, dtype=torch.float64, device="cuda")
     dest = (C.c_void_p * 1)(d1.data_ptr())
-    _check(capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, x.data_ptr(), n, y.data_ptr(), m, dest, 1, 5,
-                                                     torch.cuda.current_stream().cuda_stream))
+    _check(capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, x.data_ptr(), n, y.data_ptr(), m, dest, 1, m + 5,
+                                                     5, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
     assert torch.equal(d1[5:], y_ref) and bool((d1[:5] == -1.0).all())
+    # a destination too short for row_offset + m is rejected before anything is written
+    rc = capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, x.data_ptr(), n, y.data_ptr(), m, dest, 1, m + 4, 5,
+                                                   torch.cuda.current_stream().cuda_stream)
+    assert rc == 1 + int(sp.ErrorKind.InvalidArgument)

@@ -21,9 +21,10 @@ def _oracle_loop(oracle, m, n, r, c, v, x0, iters, normalize=False):
     for _ in range(iters):
         y = oracle.spmv(ref, 0, x)
         mass = y.sum()
+        res = np.abs(y - x).sum()  # residual ||A x_k - x_k||_1, before any rescale
         if normalize:
             y = y / mass
-        norms.append((np.abs(y - x).sum(), mass))
+        norms.append((res, mass))
         xs.append(y.copy())
         x = y
     return xs, np.array(norms)
@@ -65,7 +66,7 @@ def test_engine_iterates_within_tolerance(cuda, oracle, alg):
 
 
 def test_norms_and_leakage(cuda, oracle):
-    """norms[k] = (||x_{k+1} - x_k||_1, mass of A x_k); with empty columns the mass leaks, so it is
+    """norms[k] = (||A x_k - x_k||_1, mass of A x_k); with empty columns the mass leaks, so it is
     non-increasing for a column-(sub)stochastic matrix."""
     sp = cuda
     m, n, r, c, v = _matrix()
@@ -94,6 +95,36 @@ def test_normalized_iteration(cuda, oracle, graph):
     np.testing.assert_allclose(got, xs[30], rtol=1e-10, atol=1e-300)
     assert abs(got.sum() - 1.0) < 1e-12
     np.testing.assert_allclose(nb.cpu().numpy()[:, 1], want[:, 1], rtol=1e-10)
+    np.testing.assert_allclose(nb.cpu().numpy()[:, 0], want[:, 0], rtol=1e-9)
+
+
+@pytest.mark.parametrize("panels", [1, 3])
+@pytest.mark.parametrize("normalize", [False, True])
+def test_fused_norms_match_unfused(cuda, oracle, monkeypatch, panels, normalize):
+    """The merge engine's loop fuses the norms (and the deferred rescale) into the multiply; the
+    separate-pass loop (SPMVLAB_ITER_UNFUSED) and the oracle loop agree, with and without column
+    panels (the last panel's kernels then carry the norms)."""
+    sp = cuda
+    m, n, r, c, v = _matrix(13)
+    x0 = np.random.default_rng(6).uniform(0.0, 1.0, n) + 1e-3
+    if normalize:
+        x0 /= x0.sum()
+    xs, want = _oracle_loop(oracle, m, n, r, c, v, x0, 12, normalize=normalize)
+    monkeypatch.setenv("SPMVLAB_MERGE_PANELS", str(panels))
+    f = sp.build_format(2, sp.TripletMatrix.from_host(m, n, r, c, v), 1)
+    monkeypatch.delenv("SPMVLAB_MERGE_PANELS")
+    assert f.info["merge_panels"] == panels
+    x = torch.from_numpy(x0).cuda()
+    _, nb = sp.iterate(2, f, x, 12, normalize=normalize)
+    got, nb = x.cpu().numpy(), nb.cpu().numpy()
+    np.testing.assert_allclose(got, xs[12], rtol=2e-11, atol=1e-300)
+    np.testing.assert_allclose(nb[:, 1], want[:, 1], rtol=1e-11)
+    np.testing.assert_allclose(nb[:, 0], want[:, 0], rtol=1e-9)
+    monkeypatch.setenv("SPMVLAB_ITER_UNFUSED", "1")
+    xu = torch.from_numpy(x0).cuda()
+    _, nu = sp.iterate(2, f, xu, 12, normalize=normalize)
+    np.testing.assert_allclose(xu.cpu().numpy(), got, rtol=2e-11, atol=1e-300)
+    np.testing.assert_allclose(nu.cpu().numpy(), nb, rtol=1e-9)
 
 
 def test_graph_equals_stream_loop(cuda):
