@@ -108,9 +108,9 @@ int spmvlab_cuda_run_spmv_host(int alg, const spmvlab_cuda_format* f, const doub
  * rescaled to unit L1 mass.  If `norms` (device, 2 * iters doubles) is non-NULL, iteration k writes
  * norms[2k] = ||A x_k - x_k||_1 (the residual; = ||x_{k+1} - x_k||_1 without rescaling) and
  * norms[2k+1] = sum_i (A x_k)_i, the mass before any rescale (its drop from the previous mass is the
- * leakage through empty columns), both by deterministic fixed-order reductions.  For the merge
- * engine (2) the norms and the rescale are fused into the multiply (no extra pass over the
- * vectors; the rescale is applied lazily by the next multiply).  SPMVLAB_ITER_GRAPH captures one iteration pair (x -> work -> x) as a
+ * leakage through empty columns), both by deterministic fixed-order reductions.  One pass per
+ * iteration after the multiply computes them and (rescaling) writes A x_k back; the rescale itself
+ * is deferred to a scalar, x_{k+1} = (stored A x_k) / mass_k, and applied once at the end.  SPMVLAB_ITER_GRAPH captures one iteration pair (x -> work -> x) as a
  * CUDA graph and replays it iters / 2 times (requires a non-default stream). */
 #define SPMVLAB_ITER_NORMALIZE 1
 #define SPMVLAB_ITER_GRAPH 2

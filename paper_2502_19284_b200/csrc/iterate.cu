@@ -5,24 +5,26 @@
 // run_spmv (inc/engine.hpp:126-148).  Iteration k produces y = A x_k, the convergence norms
 // residual_k = ||A x_k - x_k||_1 and mass_k = sum(A x_k) -- with a unit-mass x_k, 1 - mass_k is the
 // leakage through empty columns of the column-normalised matrix -- and optionally rescales
-// x_{k+1} = y / mass_k to unit mass (without rescaling residual_k = ||x_{k+1} - x_k||_1).
+// x_{k+1} = A x_k / mass_k to unit mass (without rescaling residual_k = ||x_{k+1} - x_k||_1).
 //
-//  * Merge engine (the north-star engine): the norms are FUSED into the multiply.  The merge tile
-//    kernel and its carry fix-up add each row's final value into per-tile / per-warp (mass,
-//    residual) partial sums as the row is stored (one extra row-indexed read of x_k[r]), and a
-//    small reduction kernel (norms_finish_kernel) combines the partials in a fixed order.  The
-//    rescale is deferred: the stored vector is u_{k+1} = A x_k and x_{k+1} = u_{k+1} / mass_k, so
-//    iteration k + 1 multiplies u_{k+1} and scales every value it stores by 1 / mass_k (kept in
-//    device memory); the final iterate is rescaled once at the end.  No pass over the vectors
-//    besides the multiply itself.
-//  * Other engines: the multiply, then one pass over (x_k, y) for (mass, residual) and, with
-//    rescaling, one pass scaling y.
+// One pass per iteration after the multiply, with a deferred scale: the stored vector u_k and a
+// device scalar s_k with x_k = s_k u_k.  The engine multiplies the stored vector, y = A u_k, and
+// the pass reads y (and u_k for the residual) once: t = s_k y_r = (A x_k)_r is summed into the
+// mass, |t - s_k u_k[r]| into the residual, and (rescaling) t is written back, so the stored vector
+// is A x_k and s_{k+1} = 1 / mass_k.  The last iterate is scaled once at the end.  Traffic per row:
+// 24 B with rescale and norms, 16 B for either alone (two passes -- mass, then rescale -- were 32 B
+// and two launches); nothing at all when neither is asked for.
+//
+// Folding the mass and the scale into the merge kernel itself (tile partial sums of the products,
+// every stored row scaled) measured SLOWER than this pass: the latency-bound merge kernel loses an
+// occupancy step or spills with the extra registers (cfg2 loop 1.15 vs 1.12 x the multiply, cfg5
+// 1.14 vs 1.11; per-row residuals in-kernel 1.25-1.29 x).
+//
 // Reductions are deterministic: fixed per-CTA grid-stride partial sums, the last CTA to finish
-// (ticket counter) reduces the partials in a fixed tree order.
-//
-// Where the norms of iteration k go is decided on the device (an iteration counter in the scratch
-// block), so the launch parameters of every iteration pair (x -> work -> x) are identical: graph
-// mode captures ONE pair and replays it iters / 2 times.
+// (ticket counter) reduces the partials in a fixed tree order.  Where the norms of iteration k go
+// is decided on the device (an iteration counter in the scratch block), so the launch parameters of
+// every iteration pair (x -> work -> x) are identical: graph mode captures ONE pair and replays it
+// iters / 2 times.
 #include <algorithm>
 #include <string>
 #include <utility>
@@ -36,232 +38,157 @@ namespace {
 
 constexpr int kRedThreads = 256;
 constexpr unsigned kRedBlocks = 8 * kNumSMs;
-constexpr int kRedUnroll = 4;
+constexpr int kRedUnroll = 4;  // double2 per thread per step
 
 struct IterScratch {
   double partial[2 * kRedBlocks];
-  double pair[2];     // (residual, mass) of the current iteration when the caller keeps no norms
-  double inv_scale;   // fused path: x_k = stored vector * inv_scale (deferred normalisation)
-  unsigned ticket;    // CTAs finished in the current reduction
-  unsigned iter;      // iteration index (selects norms + 2 * iter)
+  double pair[2];    // (residual, mass) of the current iteration when the caller keeps no norms
+  double scale;      // s_k: x_k = scale * stored vector
+  unsigned ticket;   // CTAs finished in the current reduction
+  unsigned iter;     // iteration index (selects norms + 2 * iter)
 };
 
 __device__ __forceinline__ double* iter_out(IterScratch* sc, double* norms) {
   return norms ? norms + 2ull * sc->iter : sc->pair;
 }
 
-// MODE bit 0: accumulate the mass of y; bit 1: scale y by 1 / (mass of this iteration) first;
-// bit 2: accumulate |y - x|.  Writes out[0] = diff, out[1] = mass (those accumulated); with
-// bit 3 (last reduction of the iteration) the iteration counter advances.
-template <int MODE>
-__global__ void __launch_bounds__(kRedThreads) iter_reduce_kernel(const double* __restrict__ x,
-                                                                  double* __restrict__ y, uint64_t n,
-                                                                  IterScratch* sc, double* norms) {
-  double scale = 1.0;
-  if (MODE & 2) scale = 1.0 / iter_out(sc, norms)[1];
-  double d = 0.0, s = 0.0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (kRedUnroll - 1) * stride < n; i += kRedUnroll * stride) {
-    double v[kRedUnroll], xv[kRedUnroll];
-#pragma unroll
-    for (int u = 0; u < kRedUnroll; ++u) {
-      v[u] = y[i + u * stride];
-      if (MODE & 4) xv[u] = x[i + u * stride];
-    }
-#pragma unroll
-    for (int u = 0; u < kRedUnroll; ++u) {
-      if (MODE & 2) {
-        v[u] *= scale;
-        y[i + u * stride] = v[u];
-      }
-      if (MODE & 1) s += v[u];
-      if (MODE & 4) d += fabs(v[u] - xv[u]);
-    }
-  }
-  for (; i < n; i += stride) {
-    double v = y[i];
-    if (MODE & 2) {
-      v *= scale;
-      y[i] = v;
-    }
-    if (MODE & 1) s += v;
-    if (MODE & 4) d += fabs(v - x[i]);
-  }
-  __shared__ double sd[kRedThreads / 32], ss[kRedThreads / 32];
-  __shared__ bool last;
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  auto block_sum = [&](double& a, double& b) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_xor_sync(0xFFFFFFFFu, a, off);
-      b += __shfl_xor_sync(0xFFFFFFFFu, b, off);
-    }
-    if (lane == 0) {
-      sd[warp] = a;
-      ss[warp] = b;
-    }
-    __syncthreads();
-    a = 0.0;
-    b = 0.0;
-    for (int w = 0; w < kRedThreads / 32; ++w) {
-      a += sd[w];
-      b += ss[w];
-    }
-  };
-  block_sum(d, s);
-  if (threadIdx.x == 0) {
-    sc->partial[2 * blockIdx.x] = d;
-    sc->partial[2 * blockIdx.x + 1] = s;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double td = 0.0, ts = 0.0;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-    td += __ldcg(sc->partial + 2 * b);
-    ts += __ldcg(sc->partial + 2 * b + 1);
-  }
-  __syncthreads();  // sd / ss reuse
-  block_sum(td, ts);
-  if (threadIdx.x == 0) {
-    double* out = iter_out(sc, norms);
-    if (MODE & 4) out[0] = td;
-    if (MODE & 1) out[1] = ts;
-    sc->ticket = 0;  // ready for the next reduction (stream order)
-    if (MODE & 8) sc->iter += 1;
-  }
-}
-
-// Fused norms: the (mass, residual) partials the merge multiply left per tile and per fix-up warp,
-// reduced in a fixed order (grid-stride per thread, CTA tree, last CTA over the CTA sums).  Writes
-// out[0] = residual, out[1] = mass; with `normalize` the next iteration's deferred scale
-// inv_scale = 1 / mass; advances the iteration counter.
-__global__ void __launch_bounds__(kRedThreads) norms_finish_kernel(const double* __restrict__ tile_part,
-                                                                   uint64_t ntile, const double* __restrict__ fix_part,
-                                                                   uint64_t nfix, IterScratch* sc, double* norms,
-                                                                   int normalize) {
-  double res = 0.0, mass = 0.0;
-  const uint64_t total = ntile + nfix;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-    const double* p = i < ntile ? tile_part + 2 * i : fix_part + 2 * (i - ntile);
-    mass += p[0];
-    res += p[1];
-  }
-  __shared__ double sd[kRedThreads / 32], ss[kRedThreads / 32];
-  __shared__ bool last;
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  auto block_sum = [&](double& a, double& b) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_xor_sync(0xFFFFFFFFu, a, off);
-      b += __shfl_xor_sync(0xFFFFFFFFu, b, off);
-    }
-    if (lane == 0) {
-      sd[warp] = a;
-      ss[warp] = b;
-    }
-    __syncthreads();
-    a = 0.0;
-    b = 0.0;
-    for (int w = 0; w < kRedThreads / 32; ++w) {
-      a += sd[w];
-      b += ss[w];
-    }
-  };
-  block_sum(res, mass);
-  if (threadIdx.x == 0) {
-    sc->partial[2 * blockIdx.x] = res;
-    sc->partial[2 * blockIdx.x + 1] = mass;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double tr = 0.0, tm = 0.0;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-    tr += __ldcg(sc->partial + 2 * b);
-    tm += __ldcg(sc->partial + 2 * b + 1);
-  }
-  __syncthreads();
-  block_sum(tr, tm);
-  if (threadIdx.x == 0) {
-    double* out = iter_out(sc, norms);
-    out[0] = tr;
-    out[1] = tm;
-    if (normalize) sc->inv_scale = 1.0 / tm;
-    sc->ticket = 0;
-    sc->iter += 1;
-  }
-}
-
-// y = x * inv_scale (the fused path's final rescale; in place when y == x)
-__global__ void scale_kernel(const double* x, double* y, uint64_t n, const IterScratch* sc) {
-  const double s = sc->inv_scale;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    y[i] = x[i] * s;
-}
-
 __global__ void init_scratch_kernel(IterScratch* sc) {
-  sc->inv_scale = 1.0;
+  sc->scale = 1.0;
   sc->ticket = 0;
   sc->iter = 0;
 }
 
-// Partial-sum buffers of the fused path, sized from the last panel's tile count.
-struct FusedNorms {
-  double* tile_part = nullptr;
-  double* fix_part = nullptr;
-  uint64_t ntile = 0, nfix = 0;
-};
-
-int one_iteration_fused(const Format& f, const double* cur, double* nxt, bool normalize, double* norms,
-                        IterScratch* sc, const FusedNorms& fb, cudaStream_t s) {
-  NormCtx nc;
-  nc.xr = cur;
-  nc.inv_scale = normalize ? &sc->inv_scale : nullptr;
-  nc.tile_part = fb.tile_part;
-  nc.fix_part = fb.fix_part;
-  if (int rc = spmv_merge(f, cur, nxt, s, nullptr, &nc)) return rc;
-  const uint64_t want = (fb.ntile + fb.nfix + kRedThreads * 8 - 1) / (kRedThreads * 8);
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks, want));
-  norms_finish_kernel<<<grid, kRedThreads, 0, s>>>(fb.tile_part, fb.ntile, fb.fix_part, fb.nfix, sc, norms,
-                                                    normalize ? 1 : 0);
-  note_launch();
-  return kOk;
+// The pass after iteration k's multiply (see the file comment).  RESCALE: write t = s_k y back and
+// set s_{k+1} = 1 / mass; RESIDUAL: read u_k and accumulate |t - s_k u_k|.  Always: the mass.
+template <bool RESCALE, bool RESIDUAL>
+__global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __restrict__ u, double* __restrict__ y,
+                                                                uint64_t n, IterScratch* sc, double* norms) {
+  const double s = sc->scale;
+  double d = 0.0, m = 0.0;
+  const uint64_t n2 = n / 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double2* y2 = reinterpret_cast<double2*>(y);
+  const double2* u2 = reinterpret_cast<const double2*>(u);
+  const bool vec = ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(u)) & 15u) == 0;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto one = [&](double yv, double uv) -> double {
+    const double t = s * yv;
+    m += t;
+    if (RESIDUAL) d += fabs(t - s * uv);
+    return t;
+  };
+  if (vec) {
+    for (; i + (kRedUnroll - 1) * stride < n2; i += kRedUnroll * stride) {
+      double2 yv[kRedUnroll], uv[kRedUnroll];
+#pragma unroll
+      for (int k = 0; k < kRedUnroll; ++k) {
+        yv[k] = y2[i + k * stride];
+        if (RESIDUAL) uv[k] = __ldg(u2 + i + k * stride);
+      }
+#pragma unroll
+      for (int k = 0; k < kRedUnroll; ++k) {
+        double2 t;
+        t.x = one(yv[k].x, RESIDUAL ? uv[k].x : 0.0);
+        t.y = one(yv[k].y, RESIDUAL ? uv[k].y : 0.0);
+        if (RESCALE) y2[i + k * stride] = t;
+      }
+    }
+    for (; i < n2; i += stride) {
+      const double2 yv = y2[i];
+      const double2 uv = RESIDUAL ? __ldg(u2 + i) : make_double2(0.0, 0.0);
+      double2 t;
+      t.x = one(yv.x, uv.x);
+      t.y = one(yv.y, uv.y);
+      if (RESCALE) y2[i] = t;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {  // the odd tail element
+      const double t = one(y[n - 1], RESIDUAL ? u[n - 1] : 0.0);
+      if (RESCALE) y[n - 1] = t;
+    }
+  } else {
+    for (; i < n; i += stride) {
+      const double t = one(y[i], RESIDUAL ? u[i] : 0.0);
+      if (RESCALE) y[i] = t;
+    }
+  }
+  __shared__ double sd[kRedThreads / 32], sm[kRedThreads / 32];
+  __shared__ bool last;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  auto block_sum = [&](double& a, double& b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xFFFFFFFFu, a, off);
+      b += __shfl_xor_sync(0xFFFFFFFFu, b, off);
+    }
+    if (lane == 0) {
+      sd[warp] = a;
+      sm[warp] = b;
+    }
+    __syncthreads();
+    a = 0.0;
+    b = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) {
+      a += sd[w];
+      b += sm[w];
+    }
+  };
+  block_sum(d, m);
+  if (threadIdx.x == 0) {
+    sc->partial[2 * blockIdx.x] = d;
+    sc->partial[2 * blockIdx.x + 1] = m;
+    __threadfence();
+    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double td = 0.0, tm = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    td += __ldcg(sc->partial + 2 * b);
+    tm += __ldcg(sc->partial + 2 * b + 1);
+  }
+  __syncthreads();  // sd / sm reuse
+  block_sum(td, tm);
+  if (threadIdx.x == 0) {
+    double* out = iter_out(sc, norms);
+    out[0] = RESIDUAL ? td : 0.0;
+    out[1] = tm;
+    if (RESCALE) sc->scale = 1.0 / tm;
+    sc->ticket = 0;  // ready for the next reduction (stream order)
+    sc->iter += 1;
+  }
 }
 
-template <int MODE>
-void launch_reduce(const double* x, double* y, uint64_t n, IterScratch* sc, double* norms, cudaStream_t s) {
-  const uint64_t want = (n + (uint64_t)kRedThreads * kRedUnroll - 1) / ((uint64_t)kRedThreads * kRedUnroll);
+// y = x * scale (the last iterate, once at the end; in place when y == x)
+__global__ void scale_kernel(const double* x, double* y, uint64_t n, const IterScratch* sc) {
+  const double s = sc->scale;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] * s;
+}
+
+template <bool RESCALE, bool RESIDUAL>
+void launch_pass(const double* u, double* y, uint64_t n, IterScratch* sc, double* norms, cudaStream_t s) {
+  const uint64_t want = (n + 2ull * kRedThreads * kRedUnroll - 1) / (2ull * kRedThreads * kRedUnroll);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks, want));
-  iter_reduce_kernel<MODE><<<grid, kRedThreads, 0, s>>>(x, y, n, sc, norms);
+  iter_pass_kernel<RESCALE, RESIDUAL><<<grid, kRedThreads, 0, s>>>(u, y, n, sc, norms);
   note_launch();
 }
 
 int one_iteration(const SpmvFn& multiply, const double* cur, double* nxt, uint64_t n, bool normalize, double* norms,
                   IterScratch* sc, cudaStream_t s) {
   if (int rc = multiply(cur, nxt, s)) return rc;
-  if (normalize) {
-    launch_reduce<1 | 4>(cur, nxt, n, sc, norms, s);  // mass of A x_k and |A x_k - x_k|
-    launch_reduce<2 | 8>(cur, nxt, n, sc, norms, s);  // rescale to unit mass
-  } else if (norms) {
-    launch_reduce<1 | 4 | 8>(cur, nxt, n, sc, norms, s);
-  }
+  if (normalize && norms) launch_pass<true, true>(cur, nxt, n, sc, norms, s);
+  else if (normalize) launch_pass<true, false>(cur, nxt, n, sc, norms, s);
+  else if (norms) launch_pass<false, true>(cur, nxt, n, sc, norms, s);
   return kOk;
 }
 
 }  // namespace
 
 int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
-            double* norms, cudaStream_t s, bool fused_merge) {
+            double* norms, cudaStream_t s) {
   const uint64_t n = f.n;
   const bool normalize = flags & 1, graph = flags & 2;
-  // the fused path needs no norms pass at all; without norms or rescaling there is nothing to fuse
-  const bool fused = fused_merge && f.merge_tiles > 0 && (normalize || norms);
   IterScratch* sc = nullptr;
   if (cudaMallocAsync(&sc, sizeof(IterScratch), s) != cudaSuccess) {
     cudaGetLastError();
@@ -270,23 +197,7 @@ int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, ui
   }
   cudaMemsetAsync(sc, 0, sizeof(IterScratch), s);
   init_scratch_kernel<<<1, 1, 0, s>>>(sc);
-  FusedNorms fb;
-  if (fused) {
-    const uint32_t kl = f.merge_panels - 1;
-    fb.ntile = f.panel_tile_off[kl + 1] - f.panel_tile_off[kl];
-    fb.nfix = (fb.ntile + 31) / 32;
-    if (cudaMallocAsync(&fb.tile_part, 16 * (fb.ntile + fb.nfix + 1), s) != cudaSuccess) {
-      cudaGetLastError();
-      cudaFreeAsync(sc, s);
-      g_last_error = "device allocation failed (fused norm partials)";
-      return kNoMemory;
-    }
-    fb.fix_part = fb.tile_part + 2 * fb.ntile;
-  }
-  auto step = [&](const double* cur, double* nxt) {
-    return fused ? one_iteration_fused(f, cur, nxt, normalize, norms, sc, fb, s)
-                 : one_iteration(multiply, cur, nxt, n, normalize, norms, sc, s);
-  };
+  note_launch();
   int rc = kOk;
   uint32_t done = 0;
   if (graph && iters >= 2) {
@@ -297,8 +208,8 @@ int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, ui
     if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       rc = check_launch("iterate(capture)");
     } else {
-      rc = step(x, work);
-      if (rc == kOk) rc = step(work, x);
+      rc = one_iteration(multiply, x, work, n, normalize, norms, sc, s);
+      if (rc == kOk) rc = one_iteration(multiply, work, x, n, normalize, norms, sc, s);
       const cudaError_t ce = cudaStreamEndCapture(s, &g);
       if (rc == kOk && ce != cudaSuccess) rc = check_launch("iterate(capture)");
     }
@@ -314,17 +225,17 @@ int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, ui
   }
   double* cur = x;
   double* nxt = work;
+  if (done & 1) std::swap(cur, nxt);
   for (; rc == kOk && done < iters; ++done) {
-    rc = step(cur, nxt);
+    rc = one_iteration(multiply, cur, nxt, n, normalize, norms, sc, s);
     std::swap(cur, nxt);
   }
-  if (rc == kOk && fused && normalize && n) {  // the deferred rescale of the last iterate
+  if (rc == kOk && normalize && n) {  // x = s * stored vector (in place or into x)
     scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(cur, x, n, sc);
     note_launch();
   } else if (rc == kOk && cur != x && n) {
     cudaMemcpyAsync(x, cur, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
   }
-  if (fb.tile_part) cudaFreeAsync(fb.tile_part, s);
   cudaFreeAsync(sc, s);
   return rc ? rc : check_launch("iterate");
 }

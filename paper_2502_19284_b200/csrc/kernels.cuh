@@ -58,29 +58,16 @@ __device__ __forceinline__ void put_row(double* y, const RowDest& d, uint32_t r,
     for (unsigned i = 0; i < d.n; ++i) d.p[i][d.off + r] = v;
 }
 
-// The application loop's fused norms (iterate.cu): the merge multiply scales every stored value by
-// *inv_scale (deferred normalisation: x_k = xr * *inv_scale; null = 1) and its last panel's tiles
-// and fix-up warps leave (mass, residual) partial sums of the final rows -- sum y_r and
-// sum |y_r - x_k[r]| -- in tile_part (2 per tile) and fix_part (2 per fix-up warp).
-struct NormCtx {
-  const double* xr = nullptr;
-  const double* inv_scale = nullptr;
-  double* tile_part = nullptr;
-  double* fix_part = nullptr;
-};
-
 // ---- multiplies (stream-ordered; y fully overwritten)
 int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s);
 int spmv_par_crs(const Format& f, const double* x, double* y, cudaStream_t s);
-int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest = nullptr,
-               const NormCtx* norms = nullptr);
+int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest = nullptr);
 int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s);
 
 // ---- iterated multiply (iterate.cu): x <- A x, `iters` times, with optional norms / rescaling
 using SpmvFn = std::function<int(const double* x, double* y, cudaStream_t s)>;
-// fused_merge: f is a merge-CSR format multiplied by spmv_merge -- norms / rescale fused into it
 int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
-            double* norms, cudaStream_t s, bool fused_merge = false);
+            double* norms, cudaStream_t s);
 
 // ---- primitives
 int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,

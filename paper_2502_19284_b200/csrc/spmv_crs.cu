@@ -181,42 +181,17 @@ __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, c
 // scattered to the peers (the last panel of the fused exchange stores every row's final value).
 // (SCATTER: the peers receive the tile's finished rows in one coalesced copy at the tile end --
 // push_rows -- instead of one remote store per row per peer as the row closes)
-// NORMS (the application loop's fused norms, iterate.cu): every stored value is scaled by the
-// deferred normalisation factor, and each row's FINAL value (last panel; a tile's first row is
-// final only in tile 0 -- the others get the previous tiles' carries in the fix-up) also feeds the
-// tile's (mass, residual) sums: mass += y_r, residual += |y_r - x_k[r]| with x_k = xr * scale.
-struct NormAcc {
-  double mass = 0.0, res = 0.0, sc = 1.0;
-  uint32_t skip = 0xFFFFFFFFu;
-};
-
-template <bool SCATTER, bool ACC, bool LAST, bool NORMS>
-__device__ __forceinline__ void put_row_m(double* y, const RowDest& d, uint32_t r, double v, NormAcc& na,
-                                          const NormCtx& nc) {
-  if constexpr (NORMS) v *= na.sc;
+template <bool SCATTER, bool ACC, bool LAST>
+__device__ __forceinline__ void put_row_m(double* y, const RowDest& d, uint32_t r, double v) {
   if constexpr (ACC) v += y[r];
   put_row<false, LAST>(y, d, r, v);
-  if constexpr (NORMS && LAST) {
-    if (r != na.skip) {
-      na.mass += v;
-      na.res += fabs(v - nc.xr[r] * na.sc);
-    }
-  }
 }
 
-__device__ __forceinline__ void warp_sum2(double& a, double& b) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    a += __shfl_xor_sync(0xFFFFFFFFu, a, off);
-    b += __shfl_xor_sync(0xFFFFFFFFu, b, off);
-  }
-}
-
-template <bool SCATTER, bool ACC, bool LAST, bool NORMS>
+template <bool SCATTER, bool ACC, bool LAST>
 __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, double* __restrict__ y, uint32_t* smap,
                                          uint32_t base, uint32_t j0, uint32_t j1, uint32_t r1, uint32_t& rp,
                                          uint32_t& prevE, const double p[4], double& carry, unsigned lane,
-                                         const RowDest& dest, NormAcc& na, const NormCtx& nc) {
+                                         const RowDest& dest) {
   const uint32_t pend = min(base + 128u, j1);
   const uint32_t rp0 = rp;  // map entries <= rp0 are stale (rows closed by earlier passes) or unset
   while (rp < r1) {
@@ -228,7 +203,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
     const bool in = have && E <= pend;
     if (in) {
       if (E == S || E <= j0) {  // empty, or elements precede the tile
-        if (!ACC || SCATTER || NORMS) put_row_m<SCATTER, ACC, LAST, NORMS>(y, dest, idx, 0.0, na, nc);
+        if (!ACC || SCATTER) put_row_m<SCATTER, ACC, LAST>(y, dest, idx, 0.0);
       }
       else smap[E - 1 - base] = idx + 1u;   // closes at element E - 1 of this pass
     }
@@ -254,7 +229,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
         first_row = rid[u];
         first_val = run;
       } else {
-        put_row_m<SCATTER, ACC, LAST, NORMS>(y, dest, rid[u], run, na, nc);
+        put_row_m<SCATTER, ACC, LAST>(y, dest, rid[u], run);
       }
       run = 0.0;
     }
@@ -273,8 +248,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
   if (lane == 0) ex = 0.0;
   if (first_row >= 0)
-    put_row_m<SCATTER, ACC, LAST, NORMS>(y, dest, first_row,
-                                         first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry), na, nc);
+    put_row_m<SCATTER, ACC, LAST>(y, dest, first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
   const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
   carry = heads ? v31 : carry + v31;
   __syncwarp();
@@ -294,13 +268,12 @@ __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uin
 // 128 with two passes' loads and gathers in flight.  No product staging: shared memory holds only
 // the 128-entry row map.  LAST: the final (or only) column panel -- its stores of y are final and
 // leave the L2 with evict-first; earlier panels' partial sums are re-read by the next panel.
-template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST, bool NORMS>
-__global__ void __launch_bounds__(WARPS * 32, (NORMS ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
+template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST>
+__global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
-    double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest,
-    const __grid_constant__ NormCtx nc) {
+    double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest) {
   __shared__ __align__(16) uint32_t s_map_all[WARPS][128];
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t t = blockIdx.x * WARPS + warp;
@@ -319,11 +292,6 @@ __global__ void __launch_bounds__(WARPS * 32, (NORMS ? 40 : 48) / WARPS) merge_s
   uint32_t prevE = __ldg(row_ptr + r0);
   double carry = 0.0;
   bool more = true;
-  NormAcc na;
-  if constexpr (NORMS) {
-    na.sc = nc.inv_scale ? *nc.inv_scale : 1.0;
-    na.skip = t > 0 ? r0 : 0xFFFFFFFFu;
-  }
   for (uint32_t base = j0 & ~3u; more; base += 256u) {
     double p[2][4];
 #pragma unroll
@@ -334,21 +302,14 @@ __global__ void __launch_bounds__(WARPS * 32, (NORMS ? 40 : 48) / WARPS) merge_s
         more = false;
         break;
       }
-      vec_pass<SCATTER, ACC, LAST, NORMS>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry,
-                                          lane, dest, na, nc);
+      vec_pass<SCATTER, ACC, LAST>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane,
+                                   dest);
     }
     if (!(base + 256u < j1 || rp < r1)) more = false;
   }
   if (lane == 0) {
     carry_row[t] = r1;
-    carry_val[t] = NORMS ? carry * na.sc : carry;
-  }
-  if constexpr (NORMS && LAST) {
-    warp_sum2(na.mass, na.res);
-    if (lane == 0) {
-      nc.tile_part[2ull * t] = na.mass;
-      nc.tile_part[2ull * t + 1] = na.res;
-    }
+    carry_val[t] = carry;
   }
   if constexpr (SCATTER) {
     // rows final in this tile: [r0 + 1, r1), and row r0 too in tile 0 (every other tile's first
@@ -365,35 +326,15 @@ __global__ void __launch_bounds__(WARPS * 32, (NORMS ? 40 : 48) / WARPS) merge_s
 // starts in the chunk and continues past it is finished by the whole warp sweeping the following
 // carries 32 at a time.  Runs that started in an earlier chunk are left to that chunk's warp.
 // Deterministic (fixed reduction order) and O(run / 32) dependent steps for the longest rows.
-template <bool SCATTER, bool LAST, bool NORMS>
+template <bool SCATTER, bool LAST>
 __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
                                    const double* __restrict__ carry_val, uint32_t tiles,
-                                   double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest,
-                                   const __grid_constant__ NormCtx nc) {
+                                   double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest) {
   const unsigned lane = threadIdx.x & 31u;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t base = wid * 32u;
+  const uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
   if (base >= tiles) return;
-  const double sc = NORMS && nc.inv_scale ? *nc.inv_scale : 1.0;
-  double am = 0.0, ar = 0.0;  // NORMS: (mass, residual) of the rows this warp finalises
-  auto put = [&](uint32_t r, double v) {
-    put_row<SCATTER, LAST>(y, dest, r, v);
-    if constexpr (NORMS && LAST) {
-      am += v;
-      ar += fabs(v - nc.xr[r] * sc);
-    }
-  };
-  auto finish = [&]() {
-    if constexpr (NORMS && LAST) {
-      warp_sum2(am, ar);
-      if (lane == 0) {
-        nc.fix_part[2ull * wid] = am;
-        nc.fix_part[2ull * wid + 1] = ar;
-      }
-    }
-  };
   const uint32_t t = base + lane;
   const uint32_t r = t < tiles ? carry_row[t] : 0xFFFFFFFFu;
   double v = t < tiles ? carry_val[t] : 0.0;
@@ -409,14 +350,11 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
   }
   const bool started_here = (heads >> seg) & 1u;
   const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-  if (tail && lane != 31 && started_here && r < m) put(r, y[r] + v);
+  if (tail && lane != 31 && started_here && r < m) put_row<SCATTER, LAST>(y, dest, r, y[r] + v);
   // the chunk's last run: finish it here if it started here
   const uint32_t r31 = __shfl_sync(0xFFFFFFFFu, r, 31);
   const bool own31 = __shfl_sync(0xFFFFFFFFu, started_here, 31);
-  if (!own31 || r31 >= m) {
-    finish();
-    return;
-  }
+  if (!own31 || r31 >= m) return;
   double total = __shfl_sync(0xFFFFFFFFu, v, 31);
   for (uint32_t nb = base + 32; nb < tiles; nb += 32) {
     const uint32_t u = nb + lane;
@@ -429,8 +367,7 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
     total += w;
     if (runlen < 32) break;
   }
-  if (lane == 0) put(r31, y[r31] + total);
-  finish();
+  if (lane == 0) put_row<SCATTER, LAST>(y, dest, r31, y[r31] + total);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -456,9 +393,9 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned threads
 // Panel k of a column-panelled format (k = 0 and one panel: the plain CRS arrays), then its carry
 // fix-up.  The fix-up of panel k runs before panel k + 1's kernel (stream order; PDL waits for full
 // completion), so the accumulating panels read final sums.
-template <int IPT, bool SCATTER, bool ACC, bool LAST, bool NORMS>
+template <int IPT, bool SCATTER, bool ACC, bool LAST>
 void launch_merge_panel(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
-                        const RowDest& dest, const NormCtx& nc, uint32_t k) {
+                        const RowDest& dest, uint32_t k) {
   constexpr int WARPS = kMergeThreads / 32;
   const uint32_t t0 = f.panel_tile_off[k], tiles = f.panel_tile_off[k + 1] - t0, o = t0 + k;
   if (tiles == 0) return;
@@ -469,27 +406,26 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
   const double* val = f.find(pan ? "merge_panel_data" : "data")->as<double>();
   const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>() + o;
   const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>() + o;
-  launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST, NORMS>, (tiles + WARPS - 1) / WARPS,
-             kMergeThreads, s, rp, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest,
-             nc);
-  launch_pdl(merge_fixup_kernel<SCATTER, LAST, NORMS>, (tiles + 255) / 256, 256, s, sc->carry_row + t0,
-             (const double*)(sc->carry_val + t0), tiles, y, f.m, dest, nc);
+  launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST>, (tiles + WARPS - 1) / WARPS, kMergeThreads, s,
+             rp, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest);
+  launch_pdl(merge_fixup_kernel<SCATTER, LAST>, (tiles + 255) / 256, 256, s, sc->carry_row + t0,
+             (const double*)(sc->carry_val + t0), tiles, y, f.m, dest);
 }
 
-template <int IPT, bool NORMS>
+template <int IPT>
 void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
-                      const RowDest& dest, const NormCtx& nc, uint32_t k) {
-  const bool last = k + 1 == f.merge_panels, scatter = !NORMS && dest.n && last;
+                      const RowDest& dest, uint32_t k) {
+  const bool last = k + 1 == f.merge_panels, scatter = dest.n && last;
   if (k == 0 && last) {
-    if (scatter) launch_merge_panel<IPT, !NORMS, false, true, NORMS>(f, x, y, sc, s, dest, nc, k);
-    else launch_merge_panel<IPT, false, false, true, NORMS>(f, x, y, sc, s, dest, nc, k);
+    if (scatter) launch_merge_panel<IPT, true, false, true>(f, x, y, sc, s, dest, k);
+    else launch_merge_panel<IPT, false, false, true>(f, x, y, sc, s, dest, k);
   } else if (k == 0) {
-    launch_merge_panel<IPT, false, false, false, NORMS>(f, x, y, sc, s, dest, nc, k);
+    launch_merge_panel<IPT, false, false, false>(f, x, y, sc, s, dest, k);
   } else if (!last) {
-    launch_merge_panel<IPT, false, true, false, NORMS>(f, x, y, sc, s, dest, nc, k);
+    launch_merge_panel<IPT, false, true, false>(f, x, y, sc, s, dest, k);
   } else {
-    if (scatter) launch_merge_panel<IPT, !NORMS, true, true, NORMS>(f, x, y, sc, s, dest, nc, k);
-    else launch_merge_panel<IPT, false, true, true, NORMS>(f, x, y, sc, s, dest, nc, k);
+    if (scatter) launch_merge_panel<IPT, true, true, true>(f, x, y, sc, s, dest, k);
+    else launch_merge_panel<IPT, false, true, true>(f, x, y, sc, s, dest, k);
   }
 }
 
@@ -537,8 +473,7 @@ bool merge_shape_supported(int threads, int ipt) {
 
 // One multiply: every panel's tile kernel + carry fix-up.  The timed region (kernel timing, for the
 // roofline) spans all of them, from the first tile kernel to the last fix-up.
-int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest_in,
-               const NormCtx* norms) {
+int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, const RowDest* dest_in) {
   if (f.merge_tiles == 0) return kOk;
   RowDest dest{};
   if (dest_in) {
@@ -548,11 +483,6 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
       return kInvalidArgument;
     }
   }
-  if (norms && dest.n) {
-    g_last_error = "fused norms and the fused exchange are exclusive";
-    return kInvalidArgument;
-  }
-  const NormCtx nc = norms ? *norms : NormCtx{};
   if (!merge_shape_supported((int)f.merge_threads, (int)f.merge_ipt)) {
     g_last_error = "merge tile shape not instantiated";
     return kInvalidArgument;
@@ -564,18 +494,10 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
   }
   timing_begin("merge_spmv_vec_kernel", s);
   for (uint32_t k = 0; k < f.merge_panels; ++k) {
-    if (norms) {
-      switch (f.merge_ipt) {
-        case 8: launch_merge_ipt<8, true>(f, x, y, sc, s, dest, nc, k); break;
-        case 16: launch_merge_ipt<16, true>(f, x, y, sc, s, dest, nc, k); break;
-        default: launch_merge_ipt<32, true>(f, x, y, sc, s, dest, nc, k); break;
-      }
-    } else {
-      switch (f.merge_ipt) {
-        case 8: launch_merge_ipt<8, false>(f, x, y, sc, s, dest, nc, k); break;
-        case 16: launch_merge_ipt<16, false>(f, x, y, sc, s, dest, nc, k); break;
-        default: launch_merge_ipt<32, false>(f, x, y, sc, s, dest, nc, k); break;
-      }
+    switch (f.merge_ipt) {
+      case 8: launch_merge_ipt<8>(f, x, y, sc, s, dest, k); break;
+      case 16: launch_merge_ipt<16>(f, x, y, sc, s, dest, k); break;
+      default: launch_merge_ipt<32>(f, x, y, sc, s, dest, k); break;
     }
     if (f.panel_tile_off[k + 1] > f.panel_tile_off[k]) note_launch(2);
   }

@@ -294,8 +294,8 @@ def iterate(alg, fmt: BuiltFormat, x: torch.Tensor, iters: int, p: int = 1, norm
             graph: bool = False, norms: bool = True, work: torch.Tensor | None = None, stream=None):
     """x <- A x, `iters` times, in place on the device (the cfg5 application loop around
     inc/engine.hpp:126-148).  Returns (x, norms) with norms a (iters, 2) device tensor of
-    (||A x_k - x_k||_1, mass of A x_k) per iteration, or None (merge engine: fused into the
-    multiply, no extra pass).  graph=True runs the loop as one
+    (||A x_k - x_k||_1, mass of A x_k) per iteration, or None (one pass per iteration after the
+    multiply; the rescale is a deferred scalar).  graph=True runs the loop as one
     CUDA graph on `stream` (a torch.cuda.Stream; the current stream if None)."""
     if x.dtype != torch.float64:
         raise Error(ErrorKind.InvalidArgument, "x must be float64")

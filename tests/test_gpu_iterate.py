@@ -100,10 +100,9 @@ def test_normalized_iteration(cuda, oracle, graph):
 
 @pytest.mark.parametrize("panels", [1, 3])
 @pytest.mark.parametrize("normalize", [False, True])
-def test_fused_norms_match_unfused(cuda, oracle, monkeypatch, panels, normalize):
-    """The merge engine's loop fuses the norms (and the deferred rescale) into the multiply; the
-    separate-pass loop (SPMVLAB_ITER_UNFUSED) and the oracle loop agree, with and without column
-    panels (the last panel's kernels then carry the norms)."""
+def test_loop_norms_with_column_panels(cuda, oracle, monkeypatch, panels, normalize):
+    """The loop's one pass per iteration (deferred scale: the stored vector is A x_k, x_{k+1} =
+    stored / mass_k) against the oracle loop, on a merge format with and without column panels."""
     sp = cuda
     m, n, r, c, v = _matrix(13)
     x0 = np.random.default_rng(6).uniform(0.0, 1.0, n) + 1e-3
@@ -114,17 +113,15 @@ def test_fused_norms_match_unfused(cuda, oracle, monkeypatch, panels, normalize)
     f = sp.build_format(2, sp.TripletMatrix.from_host(m, n, r, c, v), 1)
     monkeypatch.delenv("SPMVLAB_MERGE_PANELS")
     assert f.info["merge_panels"] == panels
-    x = torch.from_numpy(x0).cuda()
-    _, nb = sp.iterate(2, f, x, 12, normalize=normalize)
-    got, nb = x.cpu().numpy(), nb.cpu().numpy()
-    np.testing.assert_allclose(got, xs[12], rtol=2e-11, atol=1e-300)
-    np.testing.assert_allclose(nb[:, 1], want[:, 1], rtol=1e-11)
-    np.testing.assert_allclose(nb[:, 0], want[:, 0], rtol=1e-9)
-    monkeypatch.setenv("SPMVLAB_ITER_UNFUSED", "1")
-    xu = torch.from_numpy(x0).cuda()
-    _, nu = sp.iterate(2, f, xu, 12, normalize=normalize)
-    np.testing.assert_allclose(xu.cpu().numpy(), got, rtol=2e-11, atol=1e-300)
-    np.testing.assert_allclose(nu.cpu().numpy(), nb, rtol=1e-9)
+    for graph in (False, True):
+        x = torch.from_numpy(x0).cuda()
+        _, nb = sp.iterate(2, f, x, 12, normalize=normalize, graph=graph)
+        got, nb = x.cpu().numpy(), nb.cpu().numpy()
+        np.testing.assert_allclose(got, xs[12], rtol=2e-11, atol=1e-300)
+        np.testing.assert_allclose(nb[:, 1], want[:, 1], rtol=1e-11)
+        np.testing.assert_allclose(nb[:, 0], want[:, 0], rtol=1e-9)
+        if normalize:
+            assert abs(got.sum() - 1.0) < 1e-12
 
 
 def test_graph_equals_stream_loop(cuda):
