@@ -454,13 +454,18 @@ def main():
 
     # dominant kernel roofline (per launch, this rank).  Algorithmic bytes of the timed kernels: the
     # reference format (storage_report) + x once + y once; with K > 1 column panels the kernels read
-    # the panel arrays instead (row pointer K m + 1 entries, the same col / data) and y is written
-    # K times and read back K - 1 times, so those are the bytes counted.
+    # the panel arrays instead (panel 0's row pointer over all m rows, the compressed pointers and
+    # row ids of panels >= 1, the same col / data) and every row of a panel >= 1 reads and writes y
+    # again, so those are the bytes counted.
     rep = sp.storage_report(fmt)
     ref_bytes = rep.total() + 8 * n + 8 * m_loc
     K = int(fmt.info["merge_panels"])
     nnz_loc = fmt.nnz()
-    alg_bytes = ref_bytes if K == 1 else (4 * (K * m_loc + 1) + 12 * nnz_loc + 8 * n + (2 * K - 1) * 8 * m_loc)
+    alg_bytes = ref_bytes
+    if K > 1:  # the panel row pointers and row ids, the entries, x, y written by panel 0 and read +
+        # written again for every row with entries in a later panel
+        ptr_b = 4 * len(fmt.array("merge_panel_row_ptr")) + 4 * len(fmt.array("merge_panel_rows"))
+        alg_bytes = ptr_b + 12 * nnz_loc + 8 * n + 8 * m_loc + 16 * int(fmt.info["merge_panel_row_visits"])
     k_ms = kms.value / max(1, kl.value)
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     kernel_name = kname.value.decode()

@@ -47,6 +47,10 @@ typedef struct {
   uint64_t l2_bytes;        /* default 512 KiB (inc/block_size.hpp:39) */
   uint64_t split_threshold; /* 0 = 2*beta (inc/spmv_parallel.hpp:205-207) */
   uint32_t build_threads;   /* accepted for interface parity; the GPU build ignores it */
+  uint32_t deterministic;   /* build option, blocked formats (3-10): bitwise-reproducible y -- every
+                               block row owned by one CTA that adds into its rows in a fixed order
+                               (the reference's exclusive rows, inc/spmv_parallel.hpp:311-350);
+                               slower than the default atomics.  The CRS engines always are. */
 } spmvlab_cuda_options;
 
 /* StorageArray (inc/storage.hpp:32-36). */
@@ -63,6 +67,7 @@ typedef struct {
   uint32_t element_level, block_level, bands;
   uint32_t merge_tiles, work_items;
   uint32_t merge_ipt, merge_panels; /* merge-CSR warp tile = 32 * merge_ipt items; column panels */
+  uint64_t merge_panel_row_visits;  /* rows with entries, summed over panels >= 1 (each re-reads y) */
 } spmvlab_cuda_format_info;
 
 int spmvlab_cuda_abi_version(void);

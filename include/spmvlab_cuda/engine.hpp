@@ -85,7 +85,8 @@ struct EngineOptions {
   std::uint64_t l2_bytes = 512 * 1024;
   std::size_t split_threshold = 0;
   unsigned build_threads = 1;
-  spmvlab_cuda_options c() const { return {l2_bytes, split_threshold, build_threads}; }
+  bool deterministic = false;  // blocked formats: bitwise-reproducible y (see spmvlab_cuda_options)
+  spmvlab_cuda_options c() const { return {l2_bytes, split_threshold, build_threads, deterministic ? 1u : 0u}; }
 };
 
 struct StorageArray {

@@ -55,7 +55,8 @@ class Coo(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("l2_bytes", C.c_uint64), ("split_threshold", C.c_uint64), ("build_threads", C.c_uint32)]
+    _fields_ = [("l2_bytes", C.c_uint64), ("split_threshold", C.c_uint64), ("build_threads", C.c_uint32),
+                ("deterministic", C.c_uint32)]
 
 
 class StorageArray(C.Structure):
@@ -67,7 +68,7 @@ class FormatInfo(C.Structure):
                 ("log2_beta", C.c_uint32), ("block_rows", C.c_uint32), ("block_cols", C.c_uint32),
                 ("element_level", C.c_uint32), ("block_level", C.c_uint32), ("bands", C.c_uint32),
                 ("merge_tiles", C.c_uint32), ("work_items", C.c_uint32),
-                ("merge_ipt", C.c_uint32), ("merge_panels", C.c_uint32)]
+                ("merge_ipt", C.c_uint32), ("merge_panels", C.c_uint32), ("merge_panel_row_visits", C.c_uint64)]
 
 
 def lib_path() -> str:

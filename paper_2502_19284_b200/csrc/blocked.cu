@@ -198,6 +198,173 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
   }
 }
 
+// Deterministic window kernel (deterministic builds, every blocked format): one CTA per WHOLE
+// block row, whose y rows it owns exclusively (the reference's exclusive rows,
+// spmv_parallel.hpp:311-350), and no atomics inside it either: every warp owns the window rows of
+// one hash bucket (32 buckets), and each batch of up to 128 elements per warp is exchanged through
+// shared memory so that warp b receives exactly the products of bucket b's rows -- per-warp bucket
+// counts (match_any ranks), a CTA scan to bucket-major offsets, a scatter of (row, product) into the
+// stage -- then warp b adds its list into its rows with plain loads and stores (equal rows inside
+// one 32-element step combined first, in lane order).  Every order is fixed, so y is the same bits
+// every run.  The price is the exchange: cfg2 CSB 1.69 ms against 0.64 ms for the CAS window
+// kernel (barrier waits and match_any; ncu r02).
+constexpr int kWbWarps = 32;
+constexpr int kWbPer = 128;                    // elements per warp per batch
+constexpr int kWbStage = kWbWarps * kWbPer;    // 4096 staged (row, product) pairs
+constexpr int kWbCntPitch = 33;                // [warp][bucket] counts, padded against bank conflicts
+
+__host__ __device__ constexpr size_t wb_smem_bytes(unsigned lb) {
+  return (sizeof(double) << lb) + kWbStage * (sizeof(double) + sizeof(uint16_t)) +
+         sizeof(uint32_t) * (kWbWarps * kWbCntPitch + 2 * kWbWarps + 2);
+}
+
+__device__ __forceinline__ uint32_t wb_bucket(uint32_t r) { return (r * 0x9E3779B1u) >> 27; }
+
+template <bool ICRS>
+__global__ void __launch_bounds__(kWbWarps * 32, 1) window_det_kernel(
+    const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc, const uint16_t* __restrict__ row_jump,
+    const double* __restrict__ data, const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
+    const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc, const uint32_t* __restrict__ item_chunk,
+    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ ord, unsigned lb, uint32_t m,
+    const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(16) uint8_t wb_smem[];
+  const uint32_t beta = 1u << lb;
+  double* win = reinterpret_cast<double*>(wb_smem);
+  double* sval = win + beta;
+  uint16_t* srow = reinterpret_cast<uint16_t*>(sval + kWbStage);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(srow + kWbStage);
+  uint32_t* bstart = cnt + kWbWarps * kWbCntPitch;  // [32 + 1]
+  uint32_t* btot = bstart + kWbWarps + 1;           // [32]
+  const uint32_t item = blockIdx.x;
+  const uint32_t c0 = item_chunk[item], c1 = item_chunk[item + 1];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint32_t i = threadIdx.x; i < beta; i += blockDim.x) win[i] = 0.0;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  // this warp's chunk stream: q = c0 + warp, c0 + warp + 32, ...
+  uint32_t q = c0 + warp, e = 0, e1 = 0, cbase = 0;
+  ChunkCoords<ICRS> cur;
+  auto open_chunk = [&]() {
+    if (q < c1) {
+      const uint32_t c = ord ? ord[q] : q;
+      e = ch_begin[c];
+      e1 = ch_begin[c + 1];
+      cbase = blk_rc[ch_blk[c]].y << lb;
+      cur = ChunkCoords<ICRS>();
+      cur.start(ch_state, c);
+    }
+  };
+  open_chunk();
+  __syncthreads();
+  bool more = true;
+  while (more) {
+    const bool have = q < c1;
+    const uint32_t bend = have ? min(e + (uint32_t)kWbPer, e1) : e;
+    uint32_t rw[4], rk[4], bk[4], cl[4];
+    double pv[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t k = e + 32u * u + lane;
+      ok[u] = have && k < bend;
+      uint32_t ir = 0, ic = 0;
+      if (__any_sync(0xFFFFFFFFu, ok[u])) cur.step(packed, col_inc, row_jump, k, ok[u], lane, lb, pf, ir, ic);
+      pv[u] = ok[u] ? ld_stream(data + k, pf) : 0.0;
+      rw[u] = ir;
+      cl[u] = ic;
+      bk[u] = wb_bucket(rw[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ok[u]) pv[u] *= ld_x(x + cbase + cl[u], pl);
+    // per-warp bucket counts and ranks
+    cnt[warp * kWbCntPitch + lane] = 0u;
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned act = __ballot_sync(0xFFFFFFFFu, ok[u]);
+      uint32_t base = 0u, mm = 0u;
+      if (ok[u]) {
+        mm = __match_any_sync(act, bk[u]);
+        base = cnt[warp * kWbCntPitch + bk[u]];
+      }
+      __syncwarp();
+      if (ok[u]) {
+        rk[u] = base + __popc(mm & lt);
+        if ((mm & lt) == 0u) cnt[warp * kWbCntPitch + bk[u]] = base + __popc(mm);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // bucket-major exclusive offsets: warp b scans bucket b's counts over the 32 warps
+    {
+      const uint32_t v = cnt[lane * kWbCntPitch + warp];
+      uint32_t inc = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+        if ((int)lane >= off) inc += t;
+      }
+      if (lane == 31) btot[warp] = inc;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t tv = btot[lane];
+        uint32_t ti = tv;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ti, off);
+          if ((int)lane >= off) ti += t;
+        }
+        bstart[lane] = ti - tv;
+        if (lane == 31) bstart[32] = ti;
+      }
+      __syncthreads();
+      cnt[lane * kWbCntPitch + warp] = bstart[warp] + inc - v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ok[u]) {
+        const uint32_t pos = cnt[warp * kWbCntPitch + bk[u]] + rk[u];
+        srow[pos] = (uint16_t)rw[u];
+        sval[pos] = pv[u];
+      }
+    __syncthreads();
+    // warp `warp` owns bucket `warp`: add its list into its window rows
+    const uint32_t beg = bstart[warp], end = bstart[warp + 1];
+    for (uint32_t j0 = beg; j0 < end; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool in = j < end;
+      const uint32_t r = in ? srow[j] : 0x10000u + lane;
+      double v = in ? sval[j] : 0.0;
+      const unsigned mm = __match_any_sync(0xFFFFFFFFu, r);
+      if (__any_sync(0xFFFFFFFFu, (mm & (mm - 1u)) != 0u)) {  // equal rows in this step: lane-order sums
+        double s = 0.0;
+        for (int t = 0; t < 32; ++t) {
+          const double vt = __shfl_sync(0xFFFFFFFFu, v, t);
+          if ((mm >> t) & 1u) s += vt;
+        }
+        v = s;
+      }
+      if (in && (mm & lt) == 0u) win[r] += v;
+      __syncwarp();
+    }
+    // advance this warp's stream
+    if (have) {
+      e = bend;
+      if (e >= e1) {
+        q += kWbWarps;
+        open_chunk();
+      }
+    }
+    more = __syncthreads_or(q < c1) != 0;
+  }
+  // the item owns its whole block row
+  const uint32_t rbase = item_br[item] << lb;
+  const uint32_t rows = min(beta, m - rbase);
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) y[rbase + i] = win[i];
+}
+
 // csb_/mergeb_/bcoh_to_triplet (csb.hpp:103-120, mergeb.hpp:110-127, bcoh.hpp:379-392): the
 // multiply's chunk walk with the coordinates stored instead of multiplied, at storage positions.
 template <bool ICRS>
@@ -275,16 +442,38 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (const DevArray* items = f.find("win_item_chunk")) {
     const uint32_t nitems = (uint32_t)(items->count() - 1);
+    const uint32_t* ord = f.find("chunk_order") ? f.find("chunk_order")->as<uint32_t>() : nullptr;
+    note_launch();
+    if (f.deterministic) {
+      const size_t smem = wb_smem_bytes(f.log2_beta);
+      once_per_device([] {
+        cudaFuncSetAttribute(window_det_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(window_det_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      });
+      const DevArray* pk = f.find("packed");
+      timing_begin("window_det_kernel", s);
+      if (icrs)
+        window_det_kernel<true><<<nitems, kWbWarps * 32, smem, s>>>(
+            nullptr, f.find("col_inc")->as<uint16_t>(), f.find("row_jump")->as<uint16_t>(), f.find("data")->as<double>(),
+            f.find("chunk_begin")->as<uint32_t>(), f.find("chunk_blk")->as<uint32_t>(),
+            f.find("chunk_state")->as<uint4>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
+            f.find("win_item_br")->as<uint32_t>(), ord, f.log2_beta, f.m, x, y);
+      else
+        window_det_kernel<false><<<nitems, kWbWarps * 32, smem, s>>>(
+            pk->as<uint32_t>(), nullptr, nullptr, f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
+            f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
+            f.find("win_item_br")->as<uint32_t>(), ord, f.log2_beta, f.m, x, y);
+      timing_end(s);
+      return check_launch("spmv_blocked(deterministic window)");
+    }
     const size_t smem = sizeof(double) << f.log2_beta;
     once_per_device(
         [] { cudaFuncSetAttribute(window_spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
-    note_launch();
     timing_begin("window_spmv_kernel", s);
     window_spmv_kernel<<<nitems, kWinThreads, smem, s>>>(
         f.find("packed")->as<uint32_t>(), f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
         f.find("chunk_blk")->as<uint32_t>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
-        f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(),
-        f.find("chunk_order") ? f.find("chunk_order")->as<uint32_t>() : nullptr, f.log2_beta, f.m, x, y);
+        f.find("win_item_br")->as<uint32_t>(), f.find("win_item_whole")->as<uint32_t>(), ord, f.log2_beta, f.m, x, y);
     timing_end(s);
     return check_launch("spmv_blocked(window)");
   }

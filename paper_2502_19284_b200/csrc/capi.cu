@@ -184,6 +184,15 @@ void* spmvlab_cuda_format::add(const std::string& name, uint64_t count, uint32_t
   return a.ptr;
 }
 
+void spmvlab_cuda_format::drop(const std::string& name) {
+  for (size_t i = 0; i < arrays.size(); ++i)
+    if (arrays[i].name == name) {
+      if (arrays[i].ptr) cudaFree(arrays[i].ptr);
+      arrays.erase(arrays.begin() + (long)i);
+      return;
+    }
+}
+
 void spmvlab_cuda_format::set_count(const std::string& name, uint64_t count) {
   if (DevArray* a = find(name)) a->bytes = count * a->esz;
 }
@@ -222,7 +231,7 @@ static int check_coo(int alg, const spmvlab_cuda_coo* a, spmvlab_cuda_format** o
 }
 
 static int build_with_beta(int alg, const spmvlab_cuda_coo* a, unsigned threads, unsigned lb, uint64_t split,
-                           spmvlab_cuda_format** out, void* stream);
+                           bool det, spmvlab_cuda_format** out, void* stream);
 
 int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threads,
                               const spmvlab_cuda_options* opt, spmvlab_cuda_format** out,
@@ -230,7 +239,8 @@ int spmvlab_cuda_build_format(int alg, const spmvlab_cuda_coo* a, unsigned threa
   if (int rc = check_coo(alg, a, out)) return rc;
   const uint64_t l2 = opt ? opt->l2_bytes : 512 * 1024;
   const uint64_t split = opt ? opt->split_threshold : 0;
-  return build_with_beta(alg, a, threads, engine_log2_beta(alg, a->n, l2), split, out, stream);
+  const bool det = opt && opt->deterministic;
+  return build_with_beta(alg, a, threads, engine_log2_beta(alg, a->n, l2), split, det, out, stream);
 }
 
 int spmvlab_cuda_build_format_beta(int alg, const spmvlab_cuda_coo* a, unsigned log2_beta, unsigned threads,
@@ -242,15 +252,16 @@ int spmvlab_cuda_build_format_beta(int alg, const spmvlab_cuda_coo* a, unsigned 
     return fail(kInvalidArgument, bcoh ? "block size outside the 15-bit increment cap"
                                        : "block size outside the 16-bit packing cap");
   if (bcoh && threads < 1) return fail(kInvalidArgument, "band count must be >= 1");
-  return build_with_beta(alg, a, threads, log2_beta, 0, out, stream);
+  return build_with_beta(alg, a, threads, log2_beta, 0, false, out, stream);
 }
 
 static int build_with_beta(int alg, const spmvlab_cuda_coo* a, unsigned threads, unsigned lb, uint64_t split,
-                           spmvlab_cuda_format** out, void* stream) {
+                           bool det, spmvlab_cuda_format** out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* f = new (std::nothrow) spmvlab_cuda_format();
   if (!f) return fail(kNoMemory, "host allocation failed");
   f->alg = alg;
+  f->deterministic = det && !is_crs_alg(alg);
   f->m = a->m;
   f->n = a->n;
   f->nnz = a->nnz;
@@ -444,6 +455,7 @@ int spmvlab_cuda_get_format_info(const spmvlab_cuda_format* f, spmvlab_cuda_form
   info->work_items = f->work_items;
   info->merge_ipt = f->merge_ipt;
   info->merge_panels = f->merge_panels;
+  info->merge_panel_row_visits = f->merge_panel_row_visits;
   return kOk;
 }
 

@@ -628,11 +628,16 @@ constexpr uint64_t kBlkPanelXBytes = 48ull << 20;
 //    block row) pair; an item owning a whole block row stores its window, the others add theirs.
 //    BCOH's Hilbert-ordered blocks interleave block rows (`permute`), so there the list is sorted
 //    even with one panel.
+//  * Deterministic builds: every blocked format gets window items, one per WHOLE block row (the
+//    chunks sorted by block row), for the bucketed window kernel -- each block row's y rows are
+//    owned by one CTA and summed in a fixed order, as the reference's exclusive rows.
 static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute = false) {
   if (f.work_items == 0) return kOk;
   cudaStream_t s = ar.stream();
   const char* env = std::getenv("SPMVLAB_BLOCKED_WINDOW");
-  const bool window = (env && env[0] ? env[0] == '1' : curve_in_block) && f.log2_beta <= 14;
+  const bool det = f.deterministic && f.log2_beta <= 14;
+  const bool window = det || ((env && env[0] ? env[0] == '1' : curve_in_block) && f.log2_beta <= 14);
+  if (det) permute = true;
   uint64_t xbytes = kBlkPanelXBytes;
   if (const char* e = std::getenv("SPMVLAB_BLK_PANEL_MB")) xbytes = (uint64_t)std::max(1, atoi(e)) << 20;
   const uint64_t want_panels = (8ull * f.n + xbytes - 1) / xbytes;
@@ -640,6 +645,7 @@ static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute
   // the per-(panel, block row) window flushes cost more than the x locality saves -- cfg3 CSB
   // 1.89 -> 2.01 ms with 48 MB panels)
   f.blk_panels = window ? 1u : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want_panels, f.block_cols));
+  if (f.deterministic && !det) f.deterministic = false;  // beta > 2^14: no shared-memory window
   const uint32_t width = (uint32_t)(((uint64_t)f.n + f.blk_panels - 1) / f.blk_panels);
   const uint32_t nch = (uint32_t)f.work_items;
   const uint32_t* ch_blk = f.find("chunk_blk")->as<uint32_t>();
@@ -663,8 +669,8 @@ static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute
   uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   if (!head || !flag) return kNoMemory;
-  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, kWinChunks, f.log2_beta, f.blk_panels,
-                                               width, head);
+  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, det ? 0xFFFFFFFFu : kWinChunks,
+                                               f.log2_beta, f.blk_panels, width, head);
   win_flag<<<(nch + 255) / 256, 256, 0, s>>>(head, nch, flag);  // flag = head != 0
   exclusive_scan_u32(flag, flag, nch, ar);                        // -> item index of each head
   uint32_t nitems = 0;
@@ -1017,7 +1023,7 @@ int build_bcoh(Format& f, const spmvlab_cuda_coo& a, unsigned lb, unsigned p, Ar
   f.arrays = sorted;
   f.nstorage = 8;
   // chunk schedule: column panels when x outgrows the L2; the Hilbert in-block (packed) variants
-  // get block-row windows over a block-row ordering of the chunks
+  // (and deterministic builds) get block-row windows over a block-row ordering of the chunks
   if (a.nnz)
     if (int rc = schedule_plan(f, ar, helem, helem)) return rc;
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_bcoh");

@@ -99,7 +99,8 @@ __global__ void panel_counts(const uint32_t* __restrict__ row_ptr, const uint32_
   }
 }
 
-// Element i of row r in panel k goes to prp[k*m + r] + (i - first element of row r in panel k).
+// Element i of row r in panel k goes to prp[k*m + r] + (i - first element of row r in panel k), that
+// first element being a binary search of the panel's first column in the row's col_ind slice.
 // One warp per 1024 consecutive elements (coalesced reads; K sequential write streams); an
 // element's row is a binary search of row_ptr between the rows of the chunk's first and last
 // elements, so rows of 10^6 entries (cfg3) are spread over many warps.
@@ -131,12 +132,43 @@ __global__ void panel_fill(const uint32_t* __restrict__ row_ptr, const uint32_t*
       const uint32_t r = row_of(row_ptr, r_lo, r_hi, i);
       const uint32_t c = col[i];
       const uint32_t k = c / width;
-      uint32_t before = 0;  // entries of row r in panels < k
-      for (uint32_t q = 0; q < k; ++q) before += prp[(uint64_t)q * m + r + 1] - prp[(uint64_t)q * m + r];
-      const uint32_t o = prp[(uint64_t)k * m + r] + (i - row_ptr[r] - before);
+      const uint32_t first = k ? row_lower_bound(col, row_ptr[r], i, (uint64_t)k * width) : row_ptr[r];
+      const uint32_t o = prp[(uint64_t)k * m + r] + (i - first);
       pcol[o] = c;
       pval[o] = val[i];
     }
+  }
+}
+
+// Panels k >= 1 that are sparse in rows are doubly compressed: only the rows with entries in the
+// panel.  flag[j] (j = (k-1) m + r) marks them, pos = its exclusive scan.  meta[k] = (offset of the
+// panel's row pointer in the concatenated pointer array, offset of its row ids, pos at the panel's
+// first row, 1 if compressed): a compressed panel's row pointer entry i and row id i go to
+// (meta.x + i, meta.y + i) with i = pos[j] - meta.z; full panels are copied separately.
+__global__ void panel_row_flags(const uint32_t* __restrict__ prp, uint32_t m, uint32_t panels,
+                                uint32_t* __restrict__ flag) {
+  const uint64_t total = (uint64_t)(panels - 1) * m;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride) {
+    const uint64_t g = j + m;  // row r of panel k = j / m + 1 in the stacked pointer
+    flag[j] = prp[g + 1] > prp[g] ? 1u : 0u;
+  }
+}
+
+__global__ void panel_row_fill(const uint32_t* __restrict__ prp, const uint32_t* __restrict__ flag,
+                               const uint32_t* __restrict__ pos, uint32_t m, uint32_t panels,
+                               const uint4* __restrict__ meta, uint32_t* __restrict__ crp,
+                               uint32_t* __restrict__ rows) {
+  const uint64_t total = (uint64_t)(panels - 1) * m;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride) {
+    if (!flag[j]) continue;
+    const uint32_t k = (uint32_t)(j / m) + 1, r = (uint32_t)(j % m);
+    const uint4 mk = meta[k];
+    if (!mk.w) continue;  // full panel
+    const uint32_t i = pos[j] - mk.z;
+    rows[mk.y + i] = r;
+    crp[mk.x + i] = prp[j + m];
   }
 }
 
@@ -229,36 +261,97 @@ int build_merge_plan(Format& f, Arena& ar) {
   uint32_t panels = 1;
   if (f.alg == kMerge && f.nnz > 0) {
     const uint64_t xb = 8ull * f.n;
-    panels = (uint32_t)std::min<uint64_t>(kMaxMergePanels, (xb + kPanelXBytes - 1) / kPanelXBytes);
+    panels = (uint32_t)std::min<uint64_t>(kAutoMergePanels, (xb + kPanelXBytes - 1) / kPanelXBytes);
     if (const char* e = getenv("SPMVLAB_MERGE_PANELS")) panels = (uint32_t)std::max(1, std::min(atoi(e), kMaxMergePanels));
     if ((uint64_t)panels * f.m + 1 > 0xFFFFFFFFull || f.n < panels) panels = 1;
   }
-  f.merge_panels = panels;
-  f.merge_panel_width = panels > 1 ? (f.n + panels - 1) / panels : f.n;
-  std::vector<uint32_t> pbase(panels + 1, 0);
-  const uint32_t* prp = nullptr;
+  std::vector<uint32_t> pbase(panels + 1, 0);   // first element of each panel in the panel arrays
+  std::vector<uint32_t> nrows(panels, f.m);     // rows the panel's merge path walks
+  std::vector<uint32_t> rp_off(panels, 0), rows_off(panels, 0);
   if (panels > 1) {
+    // The panels are an L2 optimisation: if their arrays do not fit, build without them.
     const uint64_t rows = (uint64_t)panels * f.m;
-    uint32_t* p_rp = static_cast<uint32_t*>(f.add("merge_panel_row_ptr", rows + 1, 4, s));
+    uint32_t* prp = ar.alloc_n<uint32_t>(rows + 1);
+    uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)(panels - 1) * f.m + 1);
+    uint32_t* pos = ar.alloc_n<uint32_t>((uint64_t)(panels - 1) * f.m + 1);
     uint32_t* p_col = static_cast<uint32_t*>(f.add("merge_panel_col", f.nnz, 4, s));
     double* p_val = static_cast<double*>(f.add("merge_panel_data", f.nnz, 8, s));
-    if (!p_rp || !p_col || !p_val) return kNoMemory;
-    const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
-    const uint32_t* col = f.find("col_ind")->as<uint32_t>();
-    panel_counts<<<grid_for(f.m, 256), 256, 0, s>>>(rp, col, f.m, panels, f.merge_panel_width, p_rp);
-    exclusive_scan_u32(p_rp, p_rp, rows, ar);
-    panel_fill<<<grid_for((f.nnz + 1023) / 1024 * 32, 256), 256, 0, s>>>(
-        rp, col, f.find("data")->as<double>(), f.m, f.nnz, panels, f.merge_panel_width, p_rp, p_col, p_val);
-    for (uint32_t k = 0; k <= panels; ++k)
-      cudaMemcpyAsync(&pbase[k], p_rp + (uint64_t)k * f.m, 4, cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan (panels)");
-    prp = p_rp;
-  } else {
-    pbase[1] = (uint32_t)f.nnz;
+    if (!prp || !flag || !pos || !p_col || !p_val) {
+      cudaGetLastError();
+      f.drop("merge_panel_col");
+      f.drop("merge_panel_data");
+      panels = 1;
+    } else {
+      const uint32_t width = (f.n + panels - 1) / panels;
+      const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
+      const uint32_t* col = f.find("col_ind")->as<uint32_t>();
+      panel_counts<<<grid_for(f.m, 256), 256, 0, s>>>(rp, col, f.m, panels, width, prp);
+      exclusive_scan_u32(prp, prp, rows, ar);
+      panel_fill<<<grid_for((f.nnz + 1023) / 1024 * 32, 256), 256, 0, s>>>(
+          rp, col, f.find("data")->as<double>(), f.m, f.nnz, panels, width, prp, p_col, p_val);
+      const uint64_t nflag = (uint64_t)(panels - 1) * f.m;
+      panel_row_flags<<<grid_for(nflag, 256), 256, 0, s>>>(prp, f.m, panels, flag);
+      exclusive_scan_u32(flag, pos, nflag, ar);
+      std::vector<uint32_t> pcut(panels, 0);  // pos at each panel start (k >= 1), + the total
+      for (uint32_t k = 0; k <= panels; ++k)
+        cudaMemcpyAsync(&pbase[k], prp + (uint64_t)k * f.m, 4, cudaMemcpyDeviceToHost, s);
+      for (uint32_t k = 1; k < panels; ++k)
+        cudaMemcpyAsync(&pcut[k - 1], pos + (uint64_t)(k - 1) * f.m, 4, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(&pcut[panels - 1], pos + nflag, 4, cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan (panels)");
+      // a panel with entries in more than half of the rows keeps a full row pointer (no row-id
+      // indirection: cfg4 K = 2, 97 % of the rows in panel 1, 685 -> 647 us)
+      std::vector<uint4> meta(panels, make_uint4(0, 0, 0, 0));
+      uint64_t ptr_len = (uint64_t)f.m + 1, nr = 0;
+      f.merge_panel_row_visits = pcut[panels - 1];
+      for (uint32_t k = 1; k < panels; ++k) {
+        const uint32_t rk = pcut[k] - pcut[k - 1];
+        const bool comp = (uint64_t)rk * 2 <= f.m;
+        meta[k] = make_uint4((uint32_t)ptr_len, (uint32_t)nr, pcut[k - 1], comp ? 1u : 0u);
+        nrows[k] = comp ? rk : f.m;
+        rp_off[k] = (uint32_t)ptr_len;
+        rows_off[k] = comp ? (uint32_t)nr : 0xFFFFFFFFu;
+        ptr_len += (uint64_t)nrows[k] + 1;
+        if (comp) nr += rk;
+      }
+      uint32_t* crp = static_cast<uint32_t*>(f.add("merge_panel_row_ptr", ptr_len, 4, s));
+      uint32_t* prow = static_cast<uint32_t*>(f.add("merge_panel_rows", nr, 4, s));
+      uint4* dmeta = reinterpret_cast<uint4*>(ar.alloc_n<uint32_t>(4ull * panels));
+      if (!crp || !prow || !dmeta || ptr_len > 0xFFFFFFFFull) {
+        cudaGetLastError();
+        for (const char* nm : {"merge_panel_col", "merge_panel_data", "merge_panel_row_ptr", "merge_panel_rows"})
+          f.drop(nm);
+        panels = 1;
+      } else {
+        cudaMemcpyAsync(dmeta, meta.data(), sizeof(uint4) * panels, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(crp, prp, 4ull * (f.m + 1), cudaMemcpyDeviceToDevice, s);  // panel 0: every row
+        panel_row_fill<<<grid_for(nflag, 256), 256, 0, s>>>(prp, flag, pos, f.m, panels, dmeta, crp, prow);
+        for (uint32_t k = 1; k < panels; ++k) {
+          if (meta[k].w)  // the end entry of a compressed pointer
+            cudaMemcpyAsync(crp + rp_off[k] + nrows[k], prp + (uint64_t)(k + 1) * f.m, 4, cudaMemcpyDeviceToDevice, s);
+          else            // a full panel: its slice of the stacked pointer
+            cudaMemcpyAsync(crp + rp_off[k], prp + (uint64_t)k * f.m, 4ull * (f.m + 1), cudaMemcpyDeviceToDevice, s);
+        }
+        if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_merge_plan (panel rows)");
+      }
+    }
   }
+  if (panels == 1) {
+    f.merge_panel_row_visits = 0;
+    pbase.assign(2, 0);
+    pbase[1] = (uint32_t)f.nnz;
+    nrows.assign(1, f.m);
+    rp_off.assign(1, 0);
+    rows_off.assign(1, 0);
+  }
+  f.merge_panels = panels;
+  f.merge_panel_width = panels > 1 ? (f.n + panels - 1) / panels : f.n;
+  f.panel_nrows = nrows;
+  f.panel_rp_off = rp_off;
+  f.panel_rows_off = rows_off;
   f.panel_tile_off.assign(panels + 1, 0);
   for (uint32_t k = 0; k < panels; ++k) {
-    const uint64_t tk = ((uint64_t)f.m + (pbase[k + 1] - pbase[k]) + tile_items - 1) / tile_items;
+    const uint64_t tk = ((uint64_t)nrows[k] + (pbase[k + 1] - pbase[k]) + tile_items - 1) / tile_items;
     f.panel_tile_off[k + 1] = f.panel_tile_off[k] + (uint32_t)tk;
   }
   const uint64_t tiles = f.panel_tile_off[panels];
@@ -269,12 +362,13 @@ int build_merge_plan(Format& f, Arena& ar) {
   if (!trow || !tnnz) return kNoMemory;
   // carry scratch is per stream (Format::stream_scratch); pre-create the build stream's
   if (!f.stream_scratch(s)) return kNoMemory;
+  const uint32_t* crp = panels > 1 ? f.find("merge_panel_row_ptr")->as<uint32_t>() : f.find("row_ptr")->as<uint32_t>();
   for (uint32_t k = 0; k < panels; ++k) {
     const uint32_t tk = f.panel_tile_off[k + 1] - f.panel_tile_off[k];
     const uint32_t o = f.panel_tile_off[k] + k;
     merge_partition<<<(unsigned)((tk + 1 + 255) / 256), 256, 0, s>>>(
-        panels > 1 ? prp + (uint64_t)k * f.m : f.find("row_ptr")->as<uint32_t>(), f.m,
-        (uint64_t)(pbase[k + 1] - pbase[k]), tk, tile_items, trow + o, tnnz + o, pbase[k]);
+        crp + rp_off[k], nrows[k], (uint64_t)(pbase[k + 1] - pbase[k]), tk, tile_items, trow + o, tnnz + o,
+        pbase[k]);
   }
   // ParCRS sub-warp width: next power of two >= mean row length, clamped to [2, 32]; rows longer
   // than kParLongIters * width get one CTA each.  On heavy-tailed row lengths (more than 0.1 % of

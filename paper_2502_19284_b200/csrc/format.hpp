@@ -39,9 +39,15 @@ struct spmvlab_cuda_format {
   uint32_t merge_tiles = 0;
   uint32_t merge_threads = 256, merge_ipt = 32;  // warp tile = 32 * ipt merge items
   // column panels (merge engine, x larger than the L2): panel k = columns [k*W, (k+1)*W), its
-  // tiles at merge_tile_row/nnz[panel_tile_off[k] + k ...], carries at [panel_tile_off[k] ...]
+  // tiles at merge_tile_row/nnz[panel_tile_off[k] + k ...], carries at [panel_tile_off[k] ...].
+  // Panel 0 walks all m rows (it stores y); a panel k >= 1 with entries in at most half of the
+  // rows is doubly compressed: panel_nrows[k] rows (ids at merge_panel_rows[panel_rows_off[k] ...])
+  // whose row pointer starts at merge_panel_row_ptr[panel_rp_off[k]]; the others keep a full
+  // pointer there (panel_rows_off[k] = ~0).
   uint32_t merge_panels = 1, merge_panel_width = 0;
   std::vector<uint32_t> panel_tile_off{0, 0};
+  std::vector<uint32_t> panel_nrows{0}, panel_rp_off{0}, panel_rows_off{0};
+  uint64_t merge_panel_row_visits = 0;  // rows with entries, summed over panels >= 1
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;
@@ -54,6 +60,8 @@ struct spmvlab_cuda_format {
   // column panels of the chunk schedule (x larger than the L2): chunks run panel by panel
   // ("chunk_order" / the window items), so one panel's x window stays L2-resident
   uint32_t blk_panels = 1;
+  // deterministic build (blocked formats): whole-block-row window items, the bucketed window kernel
+  bool deterministic = false;
 
   // ---- per-stream multiply scratch (merge carries), so one immutable format can serve
   // concurrent multiplies on different streams / host threads (inc/engine.hpp ownership rules).
@@ -71,6 +79,7 @@ struct spmvlab_cuda_format {
   // Allocates a named device array (16-byte padded); returns nullptr on failure.
   void* add(const std::string& name, uint64_t count, uint32_t esz, cudaStream_t s);
   void set_count(const std::string& name, uint64_t count);
+  void drop(const std::string& name);  // frees and forgets an array (no-op if absent)
 };
 
 namespace spmvcu {

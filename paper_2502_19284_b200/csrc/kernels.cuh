@@ -19,9 +19,13 @@ constexpr int kMergeIpt = 32;
 // ParCRS: rows longer than kParLongIters * group width are summed by a whole CTA (a sub-warp group
 // would walk them serially -- R-MAT s22 row 0 has ~10^5 nonzeros); those CTAs come first in the grid.
 constexpr uint32_t kParLongIters = 32;
-// Column panels of the merge engine: one panel per kPanelXBytes of x (at most kMaxMergePanels);
-// the B200 L2 is 126 MB, so x up to 96 MB runs unpanelled (R-MAT s22: 33.5 MB).
-constexpr int kMaxMergePanels = 4;
+// Column panels of the merge engine: one panel per kPanelXBytes of x, at most kAutoMergePanels by
+// default (SPMVLAB_MERGE_PANELS forces up to kMaxMergePanels); the B200 L2 is 126 MB, so x up to
+// 96 MB runs unpanelled (R-MAT s22: 33.5 MB).  B200 sweep (us per multiply, K = 1/2/3/4/6/8):
+// cfg3 1012/710/741/792/907/1025, cfg4 834/685/748/831/1016/1117, cfg5 6153/5412/5388/5447/5576/
+// 5762 -- every panel pays its rows again, so beyond 2-3 panels the x locality no longer pays.
+constexpr int kMaxMergePanels = 16;
+constexpr int kAutoMergePanels = 3;
 constexpr uint64_t kPanelXBytes = 96ull << 20;
 bool merge_shape_supported(int threads, int ipt);
 
@@ -45,6 +49,7 @@ struct RowDest {
 // LAST = false: the value is a column panel's partial sum that the next panel reads back, so it
 // is stored with the default L2 policy; the final y is written once and leaves with evict-first
 // (keeps the L2 for x: cfg3 / cfg4, x ~ L2 size: -2..3 %).
+// (evict-first for the intermediate panels too measured the same at cfg3-5: 704 / 662 / 5468 us)
 template <bool SCATTER, bool LAST = true>
 __device__ __forceinline__ void put_row(double* y, const RowDest& d, uint32_t r, double v) {
   if constexpr (LAST) {

@@ -181,17 +181,22 @@ __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, c
 // scattered to the peers (the last panel of the fused exchange stores every row's final value).
 // (SCATTER: the peers receive the tile's finished rows in one coalesced copy at the tile end --
 // push_rows -- instead of one remote store per row per peer as the row closes)
+// A doubly-compressed ACC panel walks local rows: local row r is global row rows[r].
 template <bool SCATTER, bool ACC, bool LAST>
-__device__ __forceinline__ void put_row_m(double* y, const RowDest& d, uint32_t r, double v) {
-  if constexpr (ACC) v += y[r];
+__device__ __forceinline__ void put_row_m(double* y, const uint32_t* __restrict__ rows, const RowDest& d, uint32_t r,
+                                          double v) {
+  if constexpr (ACC) {
+    if (rows) r = __ldg(rows + r);
+    v += y[r];
+  }
   put_row<false, LAST>(y, d, r, v);
 }
 
 template <bool SCATTER, bool ACC, bool LAST>
-__device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, double* __restrict__ y, uint32_t* smap,
-                                         uint32_t base, uint32_t j0, uint32_t j1, uint32_t r1, uint32_t& rp,
-                                         uint32_t& prevE, const double p[4], double& carry, unsigned lane,
-                                         const RowDest& dest) {
+__device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
+                                         double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t j0,
+                                         uint32_t j1, uint32_t r1, uint32_t& rp, uint32_t& prevE, const double p[4],
+                                         double& carry, unsigned lane, const RowDest& dest) {
   const uint32_t pend = min(base + 128u, j1);
   const uint32_t rp0 = rp;  // map entries <= rp0 are stale (rows closed by earlier passes) or unset
   while (rp < r1) {
@@ -203,7 +208,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
     const bool in = have && E <= pend;
     if (in) {
       if (E == S || E <= j0) {  // empty, or elements precede the tile
-        if (!ACC || SCATTER) put_row_m<SCATTER, ACC, LAST>(y, dest, idx, 0.0);
+        if (!ACC) put_row_m<SCATTER, ACC, LAST>(y, rows, dest, idx, 0.0);
       }
       else smap[E - 1 - base] = idx + 1u;   // closes at element E - 1 of this pass
     }
@@ -229,7 +234,7 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
         first_row = rid[u];
         first_val = run;
       } else {
-        put_row_m<SCATTER, ACC, LAST>(y, dest, rid[u], run);
+        put_row_m<SCATTER, ACC, LAST>(y, rows, dest, rid[u], run);
       }
       run = 0.0;
     }
@@ -248,7 +253,8 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, d
   double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
   if (lane == 0) ex = 0.0;
   if (first_row >= 0)
-    put_row_m<SCATTER, ACC, LAST>(y, dest, first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
+    put_row_m<SCATTER, ACC, LAST>(y, rows, dest, first_row,
+                                  first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry));
   const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
   carry = heads ? v31 : carry + v31;
   __syncwarp();
@@ -268,9 +274,14 @@ __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uin
 // 128 with two passes' loads and gathers in flight.  No product staging: shared memory holds only
 // the 128-entry row map.  LAST: the final (or only) column panel -- its stores of y are final and
 // leave the L2 with evict-first; earlier panels' partial sums are re-read by the next panel.
+// passes in flight per warp (loads and gathers of kMergeNP * 128 elements issued together; 3 passes
+// at 5 CTAs / SM measured 316 vs 289 us at cfg2, 4 spill)
+constexpr int kMergeNP = 2;
+
 template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST>
-__global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
-    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+__global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ col,
+    const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
     double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest) {
@@ -292,20 +303,20 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
   uint32_t prevE = __ldg(row_ptr + r0);
   double carry = 0.0;
   bool more = true;
-  for (uint32_t base = j0 & ~3u; more; base += 256u) {
-    double p[2][4];
+  for (uint32_t base = j0 & ~3u; more; base += 128u * kMergeNP) {
+    double p[kMergeNP][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+    for (int i = 0; i < kMergeNP; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMergeNP; ++i) {
       if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
         more = false;
         break;
       }
-      vec_pass<SCATTER, ACC, LAST>(row_ptr, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry, lane,
-                                   dest);
+      vec_pass<SCATTER, ACC, LAST>(row_ptr, rows, y, smap, base + 128u * i, j0, j1, r1, rp, prevE, p[i], carry,
+                                   lane, dest);
     }
-    if (!(base + 256u < j1 || rp < r1)) more = false;
+    if (!(base + 128u * kMergeNP < j1 || rp < r1)) more = false;
   }
   if (lane == 0) {
     carry_row[t] = r1;
@@ -326,10 +337,12 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) merge_spmv_vec_kernel(
 // starts in the chunk and continues past it is finished by the whole warp sweeping the following
 // carries 32 at a time.  Runs that started in an earlier chunk are left to that chunk's warp.
 // Deterministic (fixed reduction order) and O(run / 32) dependent steps for the longest rows.
+// (rows: the panel's compressed row ids, or null; m: the panel's row count)
 template <bool SCATTER, bool LAST>
 __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
                                    const double* __restrict__ carry_val, uint32_t tiles,
-                                   double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest) {
+                                   double* __restrict__ y, uint32_t m, const uint32_t* __restrict__ rows,
+                                   const __grid_constant__ RowDest dest) {
   const unsigned lane = threadIdx.x & 31u;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -350,7 +363,10 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
   }
   const bool started_here = (heads >> seg) & 1u;
   const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-  if (tail && lane != 31 && started_here && r < m) put_row<SCATTER, LAST>(y, dest, r, y[r] + v);
+  if (tail && lane != 31 && started_here && r < m) {
+    const uint32_t g = rows ? rows[r] : r;
+    put_row<SCATTER, LAST>(y, dest, g, y[g] + v);
+  }
   // the chunk's last run: finish it here if it started here
   const uint32_t r31 = __shfl_sync(0xFFFFFFFFu, r, 31);
   const bool own31 = __shfl_sync(0xFFFFFFFFu, started_here, 31);
@@ -367,7 +383,10 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
     total += w;
     if (runlen < 32) break;
   }
-  if (lane == 0) put_row<SCATTER, LAST>(y, dest, r31, y[r31] + total);
+  if (lane == 0) {
+    const uint32_t g = rows ? rows[r31] : r31;
+    put_row<SCATTER, LAST>(y, dest, g, y[g] + total);
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -393,6 +412,17 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned threads
 // Panel k of a column-panelled format (k = 0 and one panel: the plain CRS arrays), then its carry
 // fix-up.  The fix-up of panel k runs before panel k + 1's kernel (stream order; PDL waits for full
 // completion), so the accumulating panels read final sums.
+// Copies rows [0, m) of y to every peer (the fused exchange of a column-panelled multiply: its
+// rows are final only after the last panel's fix-up).
+__global__ void push_all_rows(const double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += stride) {
+    const double v = y[r];
+    for (unsigned i = 0; i < dest.n; ++i) dest.p[i][dest.off + r] = v;
+  }
+}
+
 template <int IPT, bool SCATTER, bool ACC, bool LAST>
 void launch_merge_panel(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
                         const RowDest& dest, uint32_t k) {
@@ -400,32 +430,40 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
   const uint32_t t0 = f.panel_tile_off[k], tiles = f.panel_tile_off[k + 1] - t0, o = t0 + k;
   if (tiles == 0) return;
   const bool pan = f.merge_panels > 1;
-  const uint32_t* rp = pan ? f.find("merge_panel_row_ptr")->as<uint32_t>() + (uint64_t)k * f.m
+  const uint32_t* rp = pan ? f.find("merge_panel_row_ptr")->as<uint32_t>() + f.panel_rp_off[k]
                            : f.find("row_ptr")->as<uint32_t>();
+  const uint32_t* rows = k > 0 && f.panel_rows_off[k] != 0xFFFFFFFFu
+                             ? f.find("merge_panel_rows")->as<uint32_t>() + f.panel_rows_off[k]
+                             : nullptr;
   const uint32_t* col = f.find(pan ? "merge_panel_col" : "col_ind")->as<uint32_t>();
   const double* val = f.find(pan ? "merge_panel_data" : "data")->as<double>();
   const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>() + o;
   const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>() + o;
   launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST>, (tiles + WARPS - 1) / WARPS, kMergeThreads, s,
-             rp, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest);
+             rp, rows, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest);
   launch_pdl(merge_fixup_kernel<SCATTER, LAST>, (tiles + 255) / 256, 256, s, sc->carry_row + t0,
-             (const double*)(sc->carry_val + t0), tiles, y, f.m, dest);
+             (const double*)(sc->carry_val + t0), tiles, y, f.panel_nrows[k], rows, dest);
 }
 
+// The tile kernels' own peer push (SCATTER) is used without panels; a panelled multiply pushes
+// all its rows after the last panel (push_all_rows).
 template <int IPT>
 void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
                       const RowDest& dest, uint32_t k) {
-  const bool last = k + 1 == f.merge_panels, scatter = dest.n && last;
+  const bool last = k + 1 == f.merge_panels;
   if (k == 0 && last) {
-    if (scatter) launch_merge_panel<IPT, true, false, true>(f, x, y, sc, s, dest, k);
+    if (dest.n) launch_merge_panel<IPT, true, false, true>(f, x, y, sc, s, dest, k);
     else launch_merge_panel<IPT, false, false, true>(f, x, y, sc, s, dest, k);
   } else if (k == 0) {
     launch_merge_panel<IPT, false, false, false>(f, x, y, sc, s, dest, k);
   } else if (!last) {
     launch_merge_panel<IPT, false, true, false>(f, x, y, sc, s, dest, k);
   } else {
-    if (scatter) launch_merge_panel<IPT, true, true, true>(f, x, y, sc, s, dest, k);
-    else launch_merge_panel<IPT, false, true, true>(f, x, y, sc, s, dest, k);
+    launch_merge_panel<IPT, false, true, true>(f, x, y, sc, s, dest, k);
+    if (dest.n) {
+      launch_pdl(push_all_rows, grid_for(f.m, 256), 256, s, (const double*)y, f.m, dest);
+      note_launch();
+    }
   }
 }
 

@@ -101,9 +101,12 @@ class EngineOptions:
     l2_bytes: int = DEFAULT_L2_BYTES
     split_threshold: int = 0
     build_threads: int = 1
+    # build option for the blocked formats: bitwise-reproducible y (exclusive block-row owners,
+    # fixed add order) instead of the faster atomics; the CRS engines always are deterministic
+    deterministic: bool = False
 
     def _c(self) -> capi.Options:
-        return capi.Options(self.l2_bytes, self.split_threshold, self.build_threads)
+        return capi.Options(self.l2_bytes, self.split_threshold, self.build_threads, int(self.deterministic))
 
 
 @dataclass

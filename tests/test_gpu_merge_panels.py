@@ -1,6 +1,6 @@
 """GPU parity: the column-panelled merge engine (x larger than the L2 -> K column panels).
 
-The panel count is chosen from 8n at build time (K = ceil(8n / 96 MiB), at most 4); here
+The panel count is chosen from 8n at build time (K = ceil(8n / 64 MiB), at most 16); here
 SPMVLAB_MERGE_PANELS forces K on small matrices so the panel paths (stacked panel CRS, per-panel
 merge tiles, accumulating kernels, per-panel carry fix-ups) are checked against the oracle at
 sizes it finishes in seconds.  The full-size configs 3-5 pick K > 1 by themselves
@@ -24,14 +24,26 @@ def _build(sp, monkeypatch, k, m, n, r, c, v, alg=2):
 
 
 def _panels_ref(m, n, k, r, c):
-    """The stacked panel row pointer restated in numpy (panel of column c = c // ceil(n / k))."""
+    """The panel row pointers and row ids restated in numpy (panel of column c = c // ceil(n / k)):
+    panel 0 over all m rows; a panel >= 1 with entries in at most half of the rows doubly
+    compressed (only those rows, plus an end entry), the others with their full pointer; offsets
+    are into the panel-major element arrays."""
     w = (n + k - 1) // k
     cnt = np.zeros(k * m, dtype=np.int64)
     np.add.at(cnt, (c.astype(np.int64) // w) * m + r.astype(np.int64), 1)
-    return np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint32)
+    stacked = np.concatenate([[0], np.cumsum(cnt)])
+    ptr, rows = [stacked[:m + 1]], [np.zeros(0, np.int64)]
+    for q in range(1, k):
+        nz = np.nonzero(cnt[q * m:(q + 1) * m])[0]
+        if 2 * len(nz) <= m:  # compressed
+            rows.append(nz)
+            ptr.append(np.concatenate([stacked[q * m + nz], [stacked[(q + 1) * m]]]))
+        else:                 # rows in more than half: the full pointer
+            ptr.append(stacked[q * m:(q + 1) * m + 1])
+    return np.concatenate(ptr).astype(np.uint32), np.concatenate(rows).astype(np.uint32)
 
 
-@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("k", [2, 3, 4, 9, 16])
 def test_panels_corpus(cuda, oracle, monkeypatch, k):
     sp = cuda
     for (m, n, r, c, v) in corpus(30, seed=31 + k):
@@ -43,7 +55,9 @@ def test_panels_corpus(cuda, oracle, monkeypatch, k):
         for name in ("row_ptr", "col_ind", "data"):  # the reference storage arrays stay bit-exact
             np.testing.assert_array_equal(f.array(name), ref.arrays[name], err_msg=name)
         if len(v) and n >= k:
-            np.testing.assert_array_equal(f.array("merge_panel_row_ptr"), _panels_ref(m, n, k, r, c))
+            want_ptr, want_rows = _panels_ref(m, n, k, r, c)
+            np.testing.assert_array_equal(f.array("merge_panel_row_ptr"), want_ptr)
+            np.testing.assert_array_equal(f.array("merge_panel_rows"), want_rows)
             # panel arrays: every entry once, panel-major then CRS order
             w = (n + k - 1) // k
             order = np.lexsort((c, r, c // w))
@@ -55,7 +69,7 @@ def test_panels_corpus(cuda, oracle, monkeypatch, k):
         np.testing.assert_array_equal(sp.run_spmv(0, f, torch.from_numpy(x).cuda(), p=1).cpu().numpy(), y_ref)
 
 
-@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("k", [2, 4, 11])
 def test_panels_long_and_empty_rows(cuda, oracle, monkeypatch, k):
     """Rows spanning many tiles in every panel, rows empty in some panels, empty rows, y preset."""
     sp = cuda
