@@ -198,9 +198,10 @@ __global__ void __launch_bounds__(kWinThreads) window_spmv_kernel(
   }
 }
 
-// Deterministic window kernel (deterministic builds, every blocked format): one CTA per WHOLE
-// block row, whose y rows it owns exclusively (the reference's exclusive rows,
-// spmv_parallel.hpp:311-350), and no atomics inside it either: every warp owns the window rows of
+// Deterministic window kernel (deterministic builds, every blocked format): one CTA per window
+// item; an item owning its whole block row stores its rows (the reference's exclusive rows,
+// spmv_parallel.hpp:311-350), a block row split over several items gets one partial window per
+// item, summed in item order by det_combine.  No atomics inside the CTA either: every warp owns the window rows of
 // one hash bucket (32 buckets), and each batch of up to 128 elements per warp is exchanged through
 // shared memory so that warp b receives exactly the products of bucket b's rows -- per-warp bucket
 // counts (match_any ranks), a CTA scan to bucket-major offsets, a scatter of (row, product) into the
@@ -225,8 +226,8 @@ __global__ void __launch_bounds__(kWbWarps * 32, 1) window_det_kernel(
     const uint32_t* __restrict__ packed, const uint16_t* __restrict__ col_inc, const uint16_t* __restrict__ row_jump,
     const double* __restrict__ data, const uint32_t* __restrict__ ch_begin, const uint32_t* __restrict__ ch_blk,
     const uint4* __restrict__ ch_state, const uint2* __restrict__ blk_rc, const uint32_t* __restrict__ item_chunk,
-    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ ord, unsigned lb, uint32_t m,
-    const double* __restrict__ x, double* __restrict__ y) {
+    const uint32_t* __restrict__ item_br, const uint32_t* __restrict__ item_slot, double* __restrict__ partials,
+    const uint32_t* __restrict__ ord, unsigned lb, uint32_t m, const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(16) uint8_t wb_smem[];
   const uint32_t beta = 1u << lb;
   double* win = reinterpret_cast<double*>(wb_smem);
@@ -359,10 +360,29 @@ __global__ void __launch_bounds__(kWbWarps * 32, 1) window_det_kernel(
     }
     more = __syncthreads_or(q < c1) != 0;
   }
-  // the item owns its whole block row
+  // an item owning its whole block row stores it; a split one fills its partial slot
   const uint32_t rbase = item_br[item] << lb;
   const uint32_t rows = min(beta, m - rbase);
-  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) y[rbase + i] = win[i];
+  const uint32_t slot = item_slot[item];
+  double* dst = slot == 0xFFFFFFFFu ? y + rbase : partials + ((uint64_t)slot << lb);
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) dst[i] = win[i];
+}
+
+// y rows of the split block rows: the partial windows of their items, added in item order.
+__global__ void det_combine(const double* __restrict__ partials, const uint32_t* __restrict__ split_br,
+                            const uint32_t* __restrict__ split_first, uint32_t nsplit, unsigned lb, uint32_t m,
+                            double* __restrict__ y) {
+  const uint32_t beta = 1u << lb;
+  const uint64_t total = (uint64_t)nsplit << lb;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+    const uint32_t b = (uint32_t)(g >> lb), i = (uint32_t)(g & (beta - 1));
+    const uint64_t row = ((uint64_t)split_br[b] << lb) + i;
+    if (row >= m) continue;
+    double s = 0.0;
+    for (uint32_t q = split_first[b]; q < split_first[b + 1]; ++q) s += partials[((uint64_t)q << lb) + i];
+    y[row] = s;
+  }
 }
 
 // csb_/mergeb_/bcoh_to_triplet (csb.hpp:103-120, mergeb.hpp:110-127, bcoh.hpp:379-392): the
@@ -451,18 +471,27 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s) {
         cudaFuncSetAttribute(window_det_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       });
       const DevArray* pk = f.find("packed");
+      const uint32_t* slot = f.find("det_item_slot")->as<uint32_t>();
+      double* part = f.find("det_partials")->as<double>();
+      const uint32_t nsplit = (uint32_t)f.find("det_split_br")->count();
       timing_begin("window_det_kernel", s);
       if (icrs)
         window_det_kernel<true><<<nitems, kWbWarps * 32, smem, s>>>(
             nullptr, f.find("col_inc")->as<uint16_t>(), f.find("row_jump")->as<uint16_t>(), f.find("data")->as<double>(),
             f.find("chunk_begin")->as<uint32_t>(), f.find("chunk_blk")->as<uint32_t>(),
             f.find("chunk_state")->as<uint4>(), f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
-            f.find("win_item_br")->as<uint32_t>(), ord, f.log2_beta, f.m, x, y);
+            f.find("win_item_br")->as<uint32_t>(), slot, part, ord, f.log2_beta, f.m, x, y);
       else
         window_det_kernel<false><<<nitems, kWbWarps * 32, smem, s>>>(
             pk->as<uint32_t>(), nullptr, nullptr, f.find("data")->as<double>(), f.find("chunk_begin")->as<uint32_t>(),
             f.find("chunk_blk")->as<uint32_t>(), nullptr, f.find("blk_rc")->as<uint2>(), items->as<uint32_t>(),
-            f.find("win_item_br")->as<uint32_t>(), ord, f.log2_beta, f.m, x, y);
+            f.find("win_item_br")->as<uint32_t>(), slot, part, ord, f.log2_beta, f.m, x, y);
+      if (nsplit) {
+        det_combine<<<grid_for((uint64_t)nsplit << f.log2_beta, 256), 256, 0, s>>>(
+            part, f.find("det_split_br")->as<uint32_t>(), f.find("det_split_first")->as<uint32_t>(), nsplit,
+            f.log2_beta, f.m, y);
+        note_launch();
+      }
       timing_end(s);
       return check_launch("spmv_blocked(deterministic window)");
     }

@@ -628,9 +628,10 @@ constexpr uint64_t kBlkPanelXBytes = 48ull << 20;
 //    block row) pair; an item owning a whole block row stores its window, the others add theirs.
 //    BCOH's Hilbert-ordered blocks interleave block rows (`permute`), so there the list is sorted
 //    even with one panel.
-//  * Deterministic builds: every blocked format gets window items, one per WHOLE block row (the
-//    chunks sorted by block row), for the bucketed window kernel -- each block row's y rows are
-//    owned by one CTA and summed in a fixed order, as the reference's exclusive rows.
+//  * Deterministic builds: every blocked format gets window items (the chunks sorted by block row)
+//    for the bucketed window kernel, which sums in a fixed order; an item owning its whole block row
+//    stores it (the reference's exclusive rows), a block row split over several items gets one
+//    partial window per item, added in item order by det_combine.
 static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute = false) {
   if (f.work_items == 0) return kOk;
   cudaStream_t s = ar.stream();
@@ -669,8 +670,8 @@ static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute
   uint32_t* head = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)nch + 1);
   if (!head || !flag) return kNoMemory;
-  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, det ? 0xFFFFFFFFu : kWinChunks,
-                                               f.log2_beta, f.blk_panels, width, head);
+  win_heads<<<(nch + 255) / 256, 256, 0, s>>>(ord, ch_blk, blk_rc, nch, kWinChunks, f.log2_beta, f.blk_panels,
+                                               width, head);
   win_flag<<<(nch + 255) / 256, 256, 0, s>>>(head, nch, flag);  // flag = head != 0
   exclusive_scan_u32(flag, flag, nch, ar);                        // -> item index of each head
   uint32_t nitems = 0;
@@ -682,6 +683,34 @@ static int schedule_plan(Format& f, Arena& ar, bool curve_in_block, bool permute
   cudaMemcpyAsync(item_chunk + nitems, &nch, 4, cudaMemcpyHostToDevice, s);
   win_fill<<<(nch + 255) / 256, 256, 0, s>>>(head, flag, ord, ch_blk, blk_rc, nch, f.blk_panels, item_chunk,
                                               item_br, item_whole);
+  if (det) {
+    // A block row split over several items: each writes its whole window to a partial slot and
+    // det_combine adds the slots in item order -- a fixed order, so still the same bits every run.
+    std::vector<uint32_t> br(nitems), whole(nitems);
+    cudaMemcpyAsync(br.data(), item_br, 4ull * nitems, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(whole.data(), item_whole, 4ull * nitems, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("schedule_plan (det)");
+    std::vector<uint32_t> slot(nitems, 0xFFFFFFFFu), sbr, sfirst;
+    uint32_t nslots = 0;
+    for (uint32_t i = 0; i < nitems; ++i) {
+      if (whole[i]) continue;
+      if (sbr.empty() || sbr.back() != br[i]) {
+        sbr.push_back(br[i]);
+        sfirst.push_back(nslots);
+      }
+      slot[i] = nslots++;
+    }
+    sfirst.push_back(nslots);
+    uint32_t* d_slot = static_cast<uint32_t*>(f.add("det_item_slot", nitems, 4, s));
+    uint32_t* d_sbr = static_cast<uint32_t*>(f.add("det_split_br", sbr.size(), 4, s));
+    uint32_t* d_sfirst = static_cast<uint32_t*>(f.add("det_split_first", sfirst.size(), 4, s));
+    double* part = static_cast<double*>(f.add("det_partials", ((uint64_t)nslots << f.log2_beta) + 1, 8, s));
+    if (!d_slot || !d_sbr || !d_sfirst || !part) return kNoMemory;
+    cudaMemcpyAsync(d_slot, slot.data(), 4ull * nitems, cudaMemcpyHostToDevice, s);
+    if (!sbr.empty()) cudaMemcpyAsync(d_sbr, sbr.data(), 4ull * sbr.size(), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_sfirst, sfirst.data(), 4ull * sfirst.size(), cudaMemcpyHostToDevice, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("schedule_plan (det)");
+  }
   return check_launch("schedule_plan");
 }
 

@@ -18,6 +18,7 @@ ap.add_argument("algs", nargs="?", default="0,1,2,3,4,5,6,7,8,9,10")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--once", action="store_true")
 ap.add_argument("--p", type=int, default=8)
+ap.add_argument("--det", action="store_true", help="deterministic builds of the blocked formats")
 args = ap.parse_args()
 name, fn = gen.CONFIGS[args.cfg]
 m, n, r, c, v = fn("cuda")
@@ -29,7 +30,7 @@ print(f"{name}: m={m} nnz={v.numel()}", flush=True)
 for alg in [int(s) for s in args.algs.split(",")]:
     torch.cuda.synchronize()
     t0 = time.time()
-    f = sp.build_format(alg, a, args.p)
+    f = sp.build_format(alg, a, args.p, sp.EngineOptions(deterministic=args.det))
     torch.cuda.synchronize()
     tb = time.time() - t0
     if args.once:
