@@ -262,8 +262,34 @@ def all_formats(sp, a, m, n, nnz, x, stream, peak, merge_us, threads=8):
     for name, d in out.items():
         t_fmt = d["spmv_us"]
         d["break_even_vs_merge"] = (d["conversion_ms"] * 1e3 / (merge_us - t_fmt)) if t_fmt < merge_us else None
+        # the paper's break-even against the row-parallel CSR baseline: multiplies
+        # after which a format's conversion is paid back by its faster SpMV
+        d["break_even_vs_parcrs"] = (d["conversion_ms"] * 1e3 / (parcrs_us - t_fmt)) if parcrs_us and t_fmt < parcrs_us else None
         d["conversion_in_parcrs_spmvs"] = d["conversion_ms"] * 1e3 / parcrs_us if parcrs_us else None
     return out
+
+
+def recorded_cpu_reference(cfg: int):
+    """The reference's own bench_spmv / bench_convert (inc/bench.hpp:239-329) recorded on a B200 box's
+    host cores by tools/cpu_reference_bench.py (profiles/cpu_reference/): per engine, the min of the
+    protocol's multiplies and conversion seconds at the highest thread count."""
+    base = os.path.join(ROOT, "profiles", "cpu_reference")
+    out = {}
+    for kind, fname in (("spmv", f"cfg{cfg}_spmv_all.json"), ("convert", f"cfg{cfg}_convert_all.json")):
+        p = os.path.join(base, fname)
+        if not os.path.exists(p):
+            continue
+        d = json.load(open(p))
+        for rec in d["records"]:
+            if rec["status"] != "ok":
+                continue
+            e = out.setdefault(rec["engine"], {"threads": rec["threads"], "host": d["host"]["cpu_model"]})
+            if kind == "spmv":
+                e["spmv_min_ms"] = rec["min_time_s"] * 1e3
+                e["spmv_reps"] = d["protocol"]["spmv_reps"]
+            else:
+                e["conversion_s"] = rec["convert_time_s"]
+    return out or None
 
 
 def main():
@@ -548,6 +574,10 @@ def main():
     if world == 1 and not args.no_formats:
         del y_host, x_host
         formats = all_formats(sp, a, m, n, nnz_total, x, stream, peak, merge_us)
+        cpu_rec = recorded_cpu_reference(args.config)
+        for name, d in (formats.items() if cpu_rec else ()):
+            if name in cpu_rec:
+                d["cpu_reference"] = cpu_rec[name]
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu:
