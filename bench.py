@@ -261,7 +261,7 @@ def all_formats(sp, a, m, n, nnz, x, stream, peak, merge_us, threads=8):
         torch.cuda.empty_cache()
     for name, d in out.items():
         t_fmt = d["spmv_us"]
-        d["break_even_vs_merge"] = (d["conversion_ms"] * 1e3 / (merge_us - t_fmt)) if t_fmt < merge_us else None
+        d["break_even_vs_merge"] = (d["conversion_ms"] * 1e3 / (merge_us - t_fmt)) if t_fmt < merge_us and name != "merge" else None
         # the paper's break-even against the row-parallel CSR baseline: multiplies
         # after which a format's conversion is paid back by its faster SpMV
         d["break_even_vs_parcrs"] = (d["conversion_ms"] * 1e3 / (parcrs_us - t_fmt)) if parcrs_us and t_fmt < parcrs_us else None
