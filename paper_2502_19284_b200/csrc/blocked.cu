@@ -123,8 +123,9 @@ __global__ void __launch_bounds__(256) blocked_spmv_kernel(
   }
 }
 
-// Block-row window kernel for CSB / MergeB (block rows are contiguous in storage): one CTA per
-// window item -- a run of chunks inside one block row -- accumulates into a beta-row y window in
+// Block-row window kernel for the curve-ordered formats (CSB, CSBH, MergeBH, BCOHCH, BCOHCHP; the
+// chunks listed by block row, through chunk_order where the storage interleaves block rows): one
+// CTA per window item -- a run of chunks inside one block row -- accumulates into a beta-row y window in
 // shared memory (shared fp64 adds, conflicts rare), then stores the window to y (item owns the
 // whole block row) or adds its nonzero entries (block row split into several items).  Replaces
 // one global fp64 reduction per element by one shared-memory add; the role of the reference's

@@ -83,13 +83,14 @@ def test_integer_exact_full_size(cuda, cfg2):
         del f
 
 
-@pytest.mark.parametrize("alg", [2, 9])
+@pytest.mark.parametrize("alg", [2, 9, 6, 4])
 def test_cfg2_pinned_to_reference(cuda, reference, cfg2, alg):
     """cfg2 pinned directly to the unmodified reference (oracle/_ref, the reference headers compiled
     by oracle/Makefile) built on this box's host cores from the same COO: every storage array of
-    CRS (triplet_to_crs, inc/crs.hpp:67-91) and MergeB (build_mergeb, inc/mergeb.hpp:50-108) bit for
-    bit; for CRS also y -- merge against the reference's spmv_merge within 1e-12 * sum|a_ij x_j|,
-    SeqCrs bitwise against spmv_crs_seq."""
+    CRS (triplet_to_crs, inc/crs.hpp:67-91), MergeB (build_mergeb, inc/mergeb.hpp:50-108), BCOHC
+    with p = host threads bands (build_bcoh, inc/bcoh.hpp:194-376) and CSBH (build_csb with the
+    Hilbert curve, inc/csb.hpp:51-100) bit for bit; for CRS also y -- merge against the reference's
+    spmv_merge within 1e-12 * sum|a_ij x_j|, SeqCrs bitwise against spmv_crs_seq."""
     sp = cuda
     m, n, r, c, v = cfg2
     rows, cols, vals = r.cpu().numpy().view(np.uint32), c.cpu().numpy().view(np.uint32), v.cpu().numpy()
