@@ -84,14 +84,24 @@ __device__ __forceinline__ uint32_t row_lower_bound(const uint32_t* __restrict__
   return b;
 }
 
+// Panel k holds the columns [cut[k], cut[k+1]) (cut[0] = 0, cut[K] = n).
+struct PanelCuts {
+  uint32_t c[kMaxMergePanels + 1];
+};
+__device__ __forceinline__ uint32_t panel_of(const PanelCuts& pc, uint32_t panels, uint32_t col) {
+  uint32_t k = 0;
+  while (k + 1 < panels && col >= pc.c[k + 1]) ++k;
+  return k;
+}
+
 __global__ void panel_counts(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t m,
-                             uint32_t panels, uint32_t width, uint32_t* __restrict__ cnt) {
+                             uint32_t panels, const __grid_constant__ PanelCuts pc, uint32_t* __restrict__ cnt) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += stride) {
     const uint32_t b = row_ptr[r], e = row_ptr[r + 1];
     uint32_t prev = b;
     for (uint32_t k = 1; k < panels; ++k) {
-      const uint32_t sp = row_lower_bound(col, prev, e, (uint64_t)k * width);
+      const uint32_t sp = row_lower_bound(col, prev, e, (uint64_t)pc.c[k]);
       cnt[(uint64_t)(k - 1) * m + r] = sp - prev;
       prev = sp;
     }
@@ -116,7 +126,8 @@ __device__ __forceinline__ uint32_t row_of(const uint32_t* __restrict__ row_ptr,
 
 __global__ void panel_fill(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
                            const double* __restrict__ val, uint32_t m, uint64_t nnz, uint32_t panels,
-                           uint32_t width, const uint32_t* __restrict__ prp, uint32_t* __restrict__ pcol,
+                           const __grid_constant__ PanelCuts pc, const uint32_t* __restrict__ prp,
+                           uint32_t* __restrict__ pcol,
                            double* __restrict__ pval) {
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -131,8 +142,8 @@ __global__ void panel_fill(const uint32_t* __restrict__ row_ptr, const uint32_t*
     for (uint32_t i = (uint32_t)e0 + lane; i < e1; i += 32) {
       const uint32_t r = row_of(row_ptr, r_lo, r_hi, i);
       const uint32_t c = col[i];
-      const uint32_t k = c / width;
-      const uint32_t first = k ? row_lower_bound(col, row_ptr[r], i, (uint64_t)k * width) : row_ptr[r];
+      const uint32_t k = panel_of(pc, panels, c);
+      const uint32_t first = k ? row_lower_bound(col, row_ptr[r], i, (uint64_t)pc.c[k]) : row_ptr[r];
       const uint32_t o = prp[(uint64_t)k * m + r] + (i - first);
       pcol[o] = c;
       pval[o] = val[i];
@@ -282,13 +293,26 @@ int build_merge_plan(Format& f, Arena& ar) {
       f.drop("merge_panel_data");
       panels = 1;
     } else {
+      // uniform column ranges; SPMVLAB_MERGE_PANEL_CUTS="c1,c2,..." (developer) sets the inner cuts
+      PanelCuts pc{};
       const uint32_t width = (f.n + panels - 1) / panels;
+      for (uint32_t k = 0; k <= panels; ++k) pc.c[k] = (uint32_t)std::min<uint64_t>((uint64_t)k * width, f.n);
+      if (const char* e = getenv("SPMVLAB_MERGE_PANEL_CUTS")) {
+        uint32_t k = 1;
+        for (const char* q = e; *q && k < panels; ++k) {
+          pc.c[k] = (uint32_t)std::min<unsigned long>(strtoul(q, nullptr, 10), f.n);
+          while (*q && *q != ',') ++q;
+          if (*q == ',') ++q;
+        }
+        for (k = 1; k < panels; ++k) pc.c[k] = std::max(pc.c[k], pc.c[k - 1]);
+      }
+      f.merge_panel_cuts.assign(pc.c, pc.c + panels + 1);
       const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
       const uint32_t* col = f.find("col_ind")->as<uint32_t>();
-      panel_counts<<<grid_for(f.m, 256), 256, 0, s>>>(rp, col, f.m, panels, width, prp);
+      panel_counts<<<grid_for(f.m, 256), 256, 0, s>>>(rp, col, f.m, panels, pc, prp);
       exclusive_scan_u32(prp, prp, rows, ar);
       panel_fill<<<grid_for((f.nnz + 1023) / 1024 * 32, 256), 256, 0, s>>>(
-          rp, col, f.find("data")->as<double>(), f.m, f.nnz, panels, width, prp, p_col, p_val);
+          rp, col, f.find("data")->as<double>(), f.m, f.nnz, panels, pc, prp, p_col, p_val);
       const uint64_t nflag = (uint64_t)(panels - 1) * f.m;
       panel_row_flags<<<grid_for(nflag, 256), 256, 0, s>>>(prp, f.m, panels, flag);
       exclusive_scan_u32(flag, pos, nflag, ar);

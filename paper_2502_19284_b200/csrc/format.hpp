@@ -48,6 +48,7 @@ struct spmvlab_cuda_format {
   std::vector<uint32_t> panel_tile_off{0, 0};
   std::vector<uint32_t> panel_nrows{0}, panel_rp_off{0}, panel_rows_off{0};
   uint64_t merge_panel_row_visits = 0;  // rows with entries, summed over panels >= 1
+  std::vector<uint32_t> merge_panel_cuts;  // panel k = columns [cuts[k], cuts[k+1])
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;
