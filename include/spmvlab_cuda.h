@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define SPMVLAB_CUDA_ABI_VERSION 2
+#define SPMVLAB_CUDA_ABI_VERSION 3
 
 /* Opaque, device-resident, immutable format (a BuiltFormat, inc/engine.hpp:82). */
 typedef struct spmvlab_cuda_format spmvlab_cuda_format;
@@ -68,6 +68,8 @@ typedef struct {
   uint32_t merge_tiles, work_items;
   uint32_t merge_ipt, merge_panels; /* merge-CSR warp tile = 32 * merge_ipt items; column panels */
   uint64_t merge_panel_row_visits;  /* rows with entries, summed over panels >= 1 (each re-reads y) */
+  uint32_t merge_hot_slots;         /* merge-CSR hot-x plan: x entries kept in shared memory (0: none) */
+  double merge_hot_share;           /* share of the nonzeros whose x is read from that copy */
 } spmvlab_cuda_format_info;
 
 int spmvlab_cuda_abi_version(void);

@@ -12,7 +12,7 @@ from .build import LIB
 
 _lib = None
 
-ABI_VERSION = 2  # SPMVLAB_CUDA_ABI_VERSION of include/spmvlab_cuda.h
+ABI_VERSION = 3  # SPMVLAB_CUDA_ABI_VERSION of include/spmvlab_cuda.h
 
 # Every symbol include/spmvlab_cuda.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = [
@@ -68,7 +68,8 @@ class FormatInfo(C.Structure):
                 ("log2_beta", C.c_uint32), ("block_rows", C.c_uint32), ("block_cols", C.c_uint32),
                 ("element_level", C.c_uint32), ("block_level", C.c_uint32), ("bands", C.c_uint32),
                 ("merge_tiles", C.c_uint32), ("work_items", C.c_uint32),
-                ("merge_ipt", C.c_uint32), ("merge_panels", C.c_uint32), ("merge_panel_row_visits", C.c_uint64)]
+                ("merge_ipt", C.c_uint32), ("merge_panels", C.c_uint32), ("merge_panel_row_visits", C.c_uint64),
+                ("merge_hot_slots", C.c_uint32), ("merge_hot_share", C.c_double)]
 
 
 def lib_path() -> str:

@@ -456,6 +456,8 @@ int spmvlab_cuda_get_format_info(const spmvlab_cuda_format* f, spmvlab_cuda_form
   info->merge_ipt = f->merge_ipt;
   info->merge_panels = f->merge_panels;
   info->merge_panel_row_visits = f->merge_panel_row_visits;
+  info->merge_hot_slots = f->merge_hot;
+  info->merge_hot_share = f->merge_hot_share;
   return kOk;
 }
 

@@ -9,12 +9,14 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace spmvcu {
+extern thread_local std::string g_last_error;
 namespace {
 
 __global__ void crs_keys(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cols,
@@ -265,7 +267,7 @@ int build_merge_plan(Format& f, Arena& ar) {
   }
   f.merge_threads = kMergeThreads;
   f.merge_ipt = ipt;
-  const uint32_t tile_items = 32u * (uint32_t)ipt;
+  uint32_t tile_items = 32u * (uint32_t)ipt;
   // Column panels for the merge engine when x outgrows the L2 (beyond ~L2 the x
   // gathers become DRAM sectors): K = ceil(8n / kPanelXBytes), at most kMaxMergePanels, so each
   // panel's x window stays L2-resident while its slice of A streams past.
@@ -368,6 +370,18 @@ int build_merge_plan(Format& f, Arena& ar) {
     rp_off.assign(1, 0);
     rows_off.assign(1, 0);
   }
+  f.merge_hot = 0;
+  f.merge_hot_share = 0.0;
+  if (panels == 1 && f.alg == kMerge) {
+    if (int rc = build_hot_columns(f, ar)) return rc;
+    if (f.merge_hot) {
+      // equal merge-path shares, kHotTilesPerWarp per warp of the persistent grid
+      uint64_t per = (uint64_t)kNumSMs * kHotWarps * kHotTilesPerWarp;
+      if (const char* e = getenv("SPMVLAB_MERGE_HOT_TILES")) per = (uint64_t)kNumSMs * kHotWarps * std::max(1, atoi(e));
+      // (at most 65535 items: the tile kernel's row map stores row - first row in 16 bits)
+      tile_items = (uint32_t)std::min<uint64_t>(65535, std::max<uint64_t>(128, (total + per - 1) / per));
+    }
+  }
   f.merge_panels = panels;
   f.merge_panel_width = panels > 1 ? (f.n + panels - 1) / panels : f.n;
   f.panel_nrows = nrows;
@@ -435,6 +449,107 @@ int build_merge_plan(Format& f, Arena& ar) {
     long_row_fill<<<(f.m + 255) / 256, 256, 0, s>>>(f.find("row_ptr")->as<uint32_t>(), f.m, lim, flag, lr);
   f.par_long = nlong;
   return check_launch("build_merge_plan");
+}
+
+// ---- hot-x plan of the merge engine (B200 design, no reference counterpart: a power-law column
+// distribution -- R-MAT -- sends a large share of the x gathers to few columns).  Columns
+// referenced at least T times, T the smallest count (>= kHotMinRefs) that keeps them within
+// kHotMaxSlots, get a shared-memory slot in column order; the plan copy merge_hot_col of col_ind
+// marks their entries 0x80000000 | slot.  Kept only when they cover kHotMinShare of the entries.
+namespace {
+__global__ void col_ref_counts(const uint32_t* __restrict__ col, uint64_t nnz, uint32_t* __restrict__ cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) atomicAdd(cnt + col[k], 1u);
+}
+
+constexpr uint32_t kRefBins = 65536;  // counts clamped to kRefBins - 1
+
+__global__ void ref_count_hist(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[1024];
+  for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t c = cnt[i];
+    if (c < 1024) atomicAdd(&sh[c], 1u);
+    else atomicAdd(hist + min(c, kRefBins - 1), 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, sh[i]);
+}
+
+__global__ void hot_flags(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t thr, uint32_t* __restrict__ flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = cnt[i] >= thr;
+}
+
+__global__ void hot_fill(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t thr, const uint32_t* __restrict__ slot,
+                         uint32_t* __restrict__ hot_cols) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && cnt[i] >= thr) hot_cols[slot[i]] = i;
+}
+
+__global__ void hot_remap(const uint32_t* __restrict__ col, uint64_t nnz, const uint32_t* __restrict__ cnt,
+                          uint32_t thr, const uint32_t* __restrict__ slot, uint32_t* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const uint32_t c = col[k];
+    out[k] = cnt[c] >= thr ? (0x80000000u | slot[c]) : c;
+  }
+}
+}  // namespace
+
+int build_hot_columns(Format& f, Arena& ar) {
+  cudaStream_t s = ar.stream();
+  f.merge_hot = 0;
+  uint32_t cap = kHotMaxSlots;
+  if (const char* e = getenv("SPMVLAB_MERGE_HOT_SLOTS")) cap = (uint32_t)std::max(0, std::min(atoi(e), (int)kHotMaxSlots));
+  if (const char* e = getenv("SPMVLAB_MERGE_HOT")) if (atoi(e) == 0) cap = 0;
+  if (cap == 0 || f.nnz == 0 || f.n == 0 || f.n > 0x7FFFFFFFu) return kOk;
+  const uint32_t* col = f.find("col_ind")->as<uint32_t>();
+  uint32_t* cnt = ar.alloc_n<uint32_t>((uint64_t)f.n + 1);
+  uint32_t* hist = ar.alloc_n<uint32_t>(kRefBins);
+  if (!cnt || !hist) return kNoMemory;
+  cudaMemsetAsync(cnt, 0, 4ull * f.n, s);
+  cudaMemsetAsync(hist, 0, 4ull * kRefBins, s);
+  col_ref_counts<<<grid_for(f.nnz, 256), 256, 0, s>>>(col, f.nnz, cnt);
+  ref_count_hist<<<grid_for(f.n, 256, kNumSMs * 4), 256, 0, s>>>(cnt, f.n, hist);
+  std::vector<uint32_t> h(kRefBins);
+  cudaMemcpyAsync(h.data(), hist, 4ull * kRefBins, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_hot_columns");
+  uint64_t take = 0, refs = 0;
+  uint32_t thr = 0;
+  for (uint32_t c = kRefBins - 1; c >= kHotMinRefs; --c) {
+    if (take + h[c] > cap) break;
+    take += h[c];
+    refs += (uint64_t)c * h[c];
+    if (h[c]) thr = c;
+  }
+  if (thr == 0 || take == 0 || (double)refs < kHotMinShare * (double)f.nnz) return check_launch("build_hot_columns");
+  uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)f.n + 1);
+  uint32_t* hc = static_cast<uint32_t*>(f.add("merge_hot_col", f.nnz, 4, s));
+  uint32_t* hl = static_cast<uint32_t*>(f.add("merge_hot_cols", take, 4, s));
+  if (!flag || !hc || !hl) {  // the hot-x plan is an optimisation: build without it
+    cudaGetLastError();
+    f.drop("merge_hot_col");
+    f.drop("merge_hot_cols");
+    return kOk;
+  }
+  hot_flags<<<grid_for(f.n, 256, 1u << 30), 256, 0, s>>>(cnt, f.n, thr, flag);
+  exclusive_scan_u32(flag, flag, f.n, ar);
+  hot_fill<<<grid_for(f.n, 256, 1u << 30), 256, 0, s>>>(cnt, f.n, thr, flag, hl);
+  hot_remap<<<grid_for(f.nnz, 256), 256, 0, s>>>(col, f.nnz, cnt, thr, flag, hc);
+  uint32_t total = 0;
+  cudaMemcpyAsync(&total, flag + f.n, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_hot_columns");
+  if (total != take) {
+    g_last_error = "hot-x plan: column count mismatch";
+    return kCudaError;
+  }
+  f.merge_hot = (uint32_t)take;
+  f.merge_hot_share = (double)refs / (double)f.nnz;
+  return check_launch("build_hot_columns");
 }
 
 int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,

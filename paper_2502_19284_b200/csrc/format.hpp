@@ -49,6 +49,10 @@ struct spmvlab_cuda_format {
   std::vector<uint32_t> panel_nrows{0}, panel_rp_off{0}, panel_rows_off{0};
   uint64_t merge_panel_row_visits = 0;  // rows with entries, summed over panels >= 1
   std::vector<uint32_t> merge_panel_cuts;  // panel k = columns [cuts[k], cuts[k+1])
+  // hot-x plan (one panel only): merge_hot x entries copied to shared memory per SM; their column
+  // indices in the plan copy "merge_hot_col" carry 0x80000000 | slot, "merge_hot_cols" lists them
+  uint32_t merge_hot = 0;
+  double merge_hot_share = 0.0;  // share of the nonzeros whose x comes from the copy
 
   // ---- ParCRS launch shape
   uint32_t par_group = 32;

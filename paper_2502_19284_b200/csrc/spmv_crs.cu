@@ -151,23 +151,38 @@ __global__ void __launch_bounds__(256) par_crs_kernel(const uint32_t* __restrict
 // 4 consecutive nonzeros of a 128-element pass per lane, loaded with one 128-bit col_ind load and
 // one 256-bit data load (sm_100 ld.global.v4.f64); the products never leave registers.  Elements
 // outside [j0, j1) are masked (the tile's merge-path element range is not 4-aligned).
+// x[c], or its shared-memory copy: with a hot-x plan the column index of the most referenced
+// columns carries 0x80000000 | slot (merge_hot_col) and sx holds x at those columns.
+template <bool HOT>
+__device__ __forceinline__ double gather_x(const double* __restrict__ x, const double* sx, uint32_t c, uint64_t pl) {
+  if constexpr (HOT) {
+    double v;
+    if ((int)c < 0) v = sx[c & 0x7FFFFFFFu];
+    else v = ld_x(x + c, pl);
+    return v;
+  } else {
+    return ld_x(x + c, pl);
+  }
+}
+
+template <bool HOT>
 __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, const double* __restrict__ val,
-                                             const double* __restrict__ x, uint32_t k, uint32_t j0, uint32_t j1,
-                                             uint64_t pf, uint64_t pl, double p[4]) {
+                                             const double* __restrict__ x, const double* sx, uint32_t k, uint32_t j0,
+                                             uint32_t j1, uint64_t pf, uint64_t pl, double p[4]) {
   if (k >= j0 && k + 3 < j1) {
     const uint4 c = ld_stream4(col + k, pf);
     double v0, v1, v2, v3;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                  : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
-    p[0] = v0 * ld_x(x + c.x, pl);
-    p[1] = v1 * ld_x(x + c.y, pl);
-    p[2] = v2 * ld_x(x + c.z, pl);
-    p[3] = v3 * ld_x(x + c.w, pl);
+    p[0] = v0 * gather_x<HOT>(x, sx, c.x, pl);
+    p[1] = v1 * gather_x<HOT>(x, sx, c.y, pl);
+    p[2] = v2 * gather_x<HOT>(x, sx, c.z, pl);
+    p[3] = v3 * gather_x<HOT>(x, sx, c.w, pl);
   } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t e = k + u;
-      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * ld_x(x + ld_stream(col + e, pf), pl) : 0.0;
+      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * gather_x<HOT>(x, sx, ld_stream(col + e, pf), pl) : 0.0;
     }
   }
 }
@@ -192,13 +207,14 @@ __device__ __forceinline__ void put_row_m(double* y, const uint32_t* __restrict_
   put_row<false, LAST>(y, d, r, v);
 }
 
+// Row ends of one pass, read 32 at a time from row_ptr and scattered to the element that closes the
+// row (smap: element - base -> row + 1); empty rows (and rows whose elements precede the tile) are
+// stored right away.
 template <bool SCATTER, bool ACC, bool LAST>
-__device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
-                                         double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t j0,
-                                         uint32_t j1, uint32_t r1, uint32_t& rp, uint32_t& prevE, const double p[4],
-                                         double& carry, unsigned lane, const RowDest& dest) {
-  const uint32_t pend = min(base + 128u, j1);
-  const uint32_t rp0 = rp;  // map entries <= rp0 are stale (rows closed by earlier passes) or unset
+__device__ __forceinline__ void row_ends(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
+                                         double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t pend,
+                                         uint32_t j0, uint32_t r1, uint32_t& rp, uint32_t& prevE, unsigned lane,
+                                         const RowDest& dest) {
   while (rp < r1) {
     const uint32_t idx = rp + lane;
     const bool have = idx < r1;
@@ -218,6 +234,51 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, c
     rp += (uint32_t)nin;
     if (nin < 32) break;
   }
+}
+
+// The same from a row window prefetched at the start of the pass group: wE = row_ptr[wb + 1 + lane]
+// for rows wb + lane < r1 (wS0 = row_ptr[wb]); rows before rp are already closed.  The window moves
+// (a dependent reload) only when all its 32 rows close within the group.
+template <bool SCATTER, bool ACC, bool LAST>
+__device__ __forceinline__ void row_ends_win(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
+                                             double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t pend,
+                                             uint32_t j0, uint32_t r1, uint32_t& rp, uint32_t& prevE, uint32_t& wb,
+                                             uint32_t& wE, uint32_t& wS0, unsigned lane, const RowDest& dest) {
+  while (rp < r1) {
+    const uint32_t idx = wb + lane;
+    uint32_t S = __shfl_up_sync(0xFFFFFFFFu, wE, 1);
+    if (lane == 0) S = wS0;
+    const bool in = idx >= rp && idx < r1 && wE <= pend;
+    if (in) {
+      if (wE == S || wE <= j0) {
+        if (!ACC) put_row_m<SCATTER, ACC, LAST>(y, rows, dest, idx, 0.0);
+      }
+      else smap[wE - 1 - base] = idx + 1u;
+    }
+    const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
+    if (inmask) {
+      prevE = __shfl_sync(0xFFFFFFFFu, wE, 31 - __clz(inmask));
+      rp += (uint32_t)__popc(inmask);
+    }
+    if (rp < wb + 32u || rp >= r1) break;
+    wb = rp;  // every row of the window closed: the next 32
+    wS0 = prevE;
+    wE = wb + lane < r1 ? __ldg(row_ptr + wb + 1 + lane) : 0xFFFFFFFFu;
+  }
+}
+
+// Each lane walks its 4 products in registers (rows closing inside the lane are stored), the lane
+// tails are combined by one warp segmented scan (carry = the open row's running sum).
+// ACC (column panels after the first): finished rows are added to y (the earlier panels' sums)
+// instead of stored; rows with no entries in the panel are left alone unless they must also be
+// scattered to the peers (the last panel of the fused exchange stores every row's final value).
+// (SCATTER: the peers receive the tile's finished rows in one coalesced copy at the tile end --
+// push_rows -- instead of one remote store per row per peer as the row closes)
+// A doubly-compressed ACC panel walks local rows: local row r is global row rows[r].
+template <bool SCATTER, bool ACC, bool LAST>
+__device__ __forceinline__ void pass_reduce(const uint32_t* __restrict__ rows, double* __restrict__ y,
+                                            const uint32_t* smap, uint32_t rp0, const double p[4], double& carry,
+                                            unsigned lane, const RowDest& dest) {
   __syncwarp();
   // Row ids only grow along the tile, so entries written by earlier passes (row + 1 <= rp0) read as
   // "no row end" and the map is never cleared (saves a 512-byte shared store per pass).
@@ -260,6 +321,17 @@ __device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, c
   __syncwarp();
 }
 
+// One 128-element pass of a warp tile: its row ends, then the reduction.
+template <bool SCATTER, bool ACC, bool LAST>
+__device__ __forceinline__ void vec_pass(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
+                                         double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t j0,
+                                         uint32_t j1, uint32_t r1, uint32_t& rp, uint32_t& prevE, const double p[4],
+                                         double& carry, unsigned lane, const RowDest& dest) {
+  const uint32_t rp0 = rp;  // map entries <= rp0 are stale (rows closed by earlier passes) or unset
+  row_ends<SCATTER, ACC, LAST>(row_ptr, rows, y, smap, base, min(base + 128u, j1), j0, r1, rp, prevE, lane, dest);
+  pass_reduce<SCATTER, ACC, LAST>(rows, y, smap, rp0, p, carry, lane, dest);
+}
+
 // The fused exchange: rows [lo, hi) of y, just finished by this warp, copied to every peer's buffer
 // at the shard's row offset -- coalesced 8-byte stores per lane, one contiguous run per peer.
 __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uint32_t lo, uint32_t hi,
@@ -278,22 +350,15 @@ __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uin
 // at 5 CTAs / SM measured 316 vs 289 us at cfg2, 4 spill)
 constexpr int kMergeNP = 2;
 
-template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST>
-__global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
-    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ col,
-    const double* __restrict__ val,
-    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
-    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
-    double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest) {
-  __shared__ __align__(16) uint32_t s_map_all[WARPS][128];
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t t = blockIdx.x * WARPS + warp;
-  // programmatic dependent launch: resident early, but no memory access before the previous
-  // kernel of the stream has completed; the fix-up behind may be launched right away
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (t >= tiles) return;
-  uint32_t* smap = s_map_all[warp];
+// One warp tile t: the merge path's items [tile_row/nnz[t], tile_row/nnz[t + 1]).
+template <bool HOT, bool SCATTER, bool ACC, bool LAST>
+__device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
+                                           const uint32_t* __restrict__ col, const double* __restrict__ val,
+                                           const double* __restrict__ x, const double* sx, double* __restrict__ y,
+                                           const uint32_t* __restrict__ tile_row,
+                                           const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+                                           double* __restrict__ carry_val, uint32_t t, uint32_t* smap,
+                                           unsigned lane, const RowDest& dest) {
   *reinterpret_cast<uint4*>(smap + 4 * lane) = make_uint4(0u, 0u, 0u, 0u);
   const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
@@ -303,10 +368,12 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
   uint32_t prevE = __ldg(row_ptr + r0);
   double carry = 0.0;
   bool more = true;
+  __syncwarp();
   for (uint32_t base = j0 & ~3u; more; base += 128u * kMergeNP) {
     double p[kMergeNP][4];
 #pragma unroll
-    for (int i = 0; i < kMergeNP; ++i) vec_products(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+    for (int i = 0; i < kMergeNP; ++i)
+      vec_products<HOT>(col, val, x, sx, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
 #pragma unroll
     for (int i = 0; i < kMergeNP; ++i) {
       if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
@@ -328,6 +395,212 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
     __syncwarp();
     push_rows(y, dest, t == 0 ? r0 : r0 + 1u, r1, lane);
   }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- persistent 8-wide tiles
+// The persistent kernels walk a tile in passes of 256 elements, 8 consecutive ones per lane: one
+// 256-bit col_ind load and two 256-bit data loads (L2 evict-first as an instruction qualifier --
+// no policy register), one row-map round trip and one warp segmented scan per 256 elements (half
+// the merge instructions per element of the 4-wide passes).  Software pipelined: col_ind of the
+// next pass is loaded one pass ahead, and the row window (row_ptr of the next 32 rows) is loaded
+// with the pass's data and x gathers, so a pass costs about one memory latency instead of three
+// in series (col -> x, then row_ptr).
+struct Cols8 {
+  uint32_t c[8];
+};
+
+__device__ __forceinline__ Cols8 cols8(const uint32_t* __restrict__ col, uint32_t k, uint32_t j0, uint32_t j1) {
+  Cols8 r;
+  if (k >= j0 && k + 7 < j1) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.c[0]), "=r"(r.c[1]), "=r"(r.c[2]), "=r"(r.c[3]), "=r"(r.c[4]), "=r"(r.c[5]),
+                   "=r"(r.c[6]), "=r"(r.c[7])
+                 : "l"(col + k));
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r.c[u] = (k + u >= j0 && k + u < j1) ? __ldg(col + k + u) : 0u;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void ld_val4(const double* p, double v[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+template <bool HOT>
+__device__ __forceinline__ void products8(const double* __restrict__ val, const double* __restrict__ x,
+                                          const double* sx, const Cols8& c, uint32_t k, uint32_t j0, uint32_t j1,
+                                          uint64_t pl, double p[8]) {
+  if (k >= j0 && k + 7 < j1) {
+    double v[8];
+    ld_val4(val + k, v);
+    ld_val4(val + k + 4, v + 4);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = v[u] * gather_x<HOT>(x, sx, c.c[u], pl);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t e = k + u;
+      p[u] = (e >= j0 && e < j1) ? __ldg(val + e) * gather_x<HOT>(x, sx, c.c[u], pl) : 0.0;
+    }
+  }
+}
+
+// y stores of the persistent kernels: final values, L2 evict-first (policy made once per tile)
+__device__ __forceinline__ void st_y(double* y, uint32_t r, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(y + r), "d"(v), "l"(pol) : "memory");
+}
+
+template <bool SCATTER>
+__device__ __forceinline__ void row_ends8(const uint32_t* __restrict__ row_ptr, double* __restrict__ y,
+                                          uint16_t* smap, uint32_t r0, uint32_t base, uint32_t pend, uint32_t j0,
+                                          uint32_t r1,
+                                          uint32_t& rp, uint32_t& prevE, uint32_t& wb, uint32_t& wE, uint32_t& wS0,
+                                          unsigned lane, uint64_t ps) {
+  while (rp < r1) {
+    const uint32_t idx = wb + lane;
+    uint32_t S = __shfl_up_sync(0xFFFFFFFFu, wE, 1);
+    if (lane == 0) S = wS0;
+    const bool in = idx >= rp && idx < r1 && wE <= pend;
+    if (in && (wE == S || wE <= j0)) st_y(y, idx, 0.0, ps);  // empty, or elements precede the tile
+    else if (in) smap[wE - 1 - base] = (uint16_t)(idx - r0 + 1u);  // closes at element wE - 1 of the pass
+    const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
+    if (inmask) {
+      prevE = __shfl_sync(0xFFFFFFFFu, wE, 31 - __clz(inmask));
+      rp += (uint32_t)__popc(inmask);
+    }
+    if (rp < wb + 32u || rp >= r1) break;
+    wb = rp;  // every row of the window closed: the next 32
+    wS0 = prevE;
+    wE = wb + lane < r1 ? __ldg(row_ptr + wb + 1 + lane) : 0xFFFFFFFFu;
+  }
+}
+
+// (the row map holds row - r0 + 1 as 16 bits: a tile spans at most 65535 rows, build_merge_plan)
+__device__ __forceinline__ void reduce8(double* __restrict__ y, const uint16_t* smap, uint32_t r0, uint32_t rp0,
+                                        const double p[8], double& carry, unsigned lane, uint64_t ps) {
+  __syncwarp();
+  const uint4 mq = *reinterpret_cast<const uint4*>(smap + 8 * lane);
+  const uint32_t mm[8] = {mq.x & 0xFFFFu, mq.x >> 16, mq.y & 0xFFFFu, mq.y >> 16,
+                          mq.z & 0xFFFFu, mq.z >> 16, mq.w & 0xFFFFu, mq.w >> 16};
+  const uint32_t stale = rp0 - r0;  // entries <= stale: rows closed by earlier passes, or unset
+  double run = 0.0, first_val = 0.0;
+  int first_row = -1;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    run += p[u];
+    const bool end = mm[u] > stale;
+    if (end && first_row >= 0) st_y(y, r0 + mm[u] - 1u, run, ps);
+    if (end && first_row < 0) {
+      first_row = (int)(r0 + mm[u] - 1u);
+      first_val = run;
+    }
+    run = end ? 0.0 : run;
+  }
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, first_row >= 0);
+  const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+  const int seg = heads & le ? 31 - __clz(heads & le) : 0;
+  double v = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ov = __shfl_up_sync(0xFFFFFFFFu, v, off);
+    v += ((int)lane - off >= seg) ? ov : 0.0;
+  }
+  double ex = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+  if (lane == 0) ex = 0.0;
+  if (first_row >= 0)
+    st_y(y, (uint32_t)first_row, first_val + ex + ((heads & ((1u << lane) - 1u)) ? 0.0 : carry), ps);
+  const double v31 = __shfl_sync(0xFFFFFFFFu, v, 31);
+  carry = heads ? v31 : carry + v31;
+  __syncwarp();
+}
+
+template <bool HOT, bool SCATTER>
+__device__ __forceinline__ void merge_tile8(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                                            const double* __restrict__ val, const double* __restrict__ x,
+                                            const double* sx, double* __restrict__ y,
+                                            const uint32_t* __restrict__ tile_row,
+                                            const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+                                            double* __restrict__ carry_val, uint32_t t, uint16_t* smap,
+                                            unsigned lane, const RowDest& dest, uint64_t pl, uint64_t ps) {
+  *reinterpret_cast<uint4*>(smap + 8 * lane) = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+  const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
+  uint32_t rp = r0;
+  uint32_t prevE = __ldg(row_ptr + r0);
+  double carry = 0.0;
+  uint32_t base = j0 & ~7u;
+  Cols8 cn = cols8(col, base + 8 * lane, j0, j1);
+  __syncwarp();
+  while (base < j1 || rp < r1) {
+    uint32_t wb = rp, wS0 = prevE;
+    uint32_t wE = rp + lane < r1 ? __ldg(row_ptr + rp + 1 + lane) : 0xFFFFFFFFu;
+    double p[8];
+    products8<HOT>(val, x, sx, cn, base + 8 * lane, j0, j1, pl, p);
+    cn = cols8(col, base + 256u + 8 * lane, j0, j1);
+    const uint32_t rp0 = rp;
+    row_ends8<SCATTER>(row_ptr, y, smap, r0, base, min(base + 256u, j1), j0, r1, rp, prevE, wb, wE, wS0, lane, ps);
+    reduce8(y, smap, r0, rp0, p, carry, lane, ps);
+    base += 256u;
+  }
+  if (lane == 0) {
+    carry_row[t] = r1;
+    carry_val[t] = carry;
+  }
+  if constexpr (SCATTER) {
+    // rows final in this tile: [r0 + 1, r1), and row r0 too in tile 0 (every other tile's first
+    // row receives the previous tiles' carries in the fix-up, which pushes it)
+    __syncwarp();
+    push_rows(y, dest, t == 0 ? r0 : r0 + 1u, r1, lane);
+  }
+  __syncwarp();
+}
+
+template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST>
+__global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ col,
+    const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
+    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
+    double* __restrict__ carry_val, uint32_t tiles, const __grid_constant__ RowDest dest) {
+  __shared__ __align__(16) uint32_t s_map_all[WARPS][128];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x * WARPS + warp;
+  // programmatic dependent launch: resident early, but no memory access before the previous
+  // kernel of the stream has completed; the fix-up behind may be launched right away
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (t >= tiles) return;
+  merge_tile<false, SCATTER, ACC, LAST>(row_ptr, rows, col, val, x, nullptr, y, tile_row, tile_nnz, carry_row,
+                                        carry_val, t, s_map_all[warp], lane, dest);
+}
+
+// Hot-x variant (R-MAT-like column skew; plan built by build_hot_columns): one persistent CTA of
+// kHotWarps warps per SM.  The CTA first copies x at the plan's hot columns (merge_hot_cols, the
+// most referenced ones) into shared memory; its warps then walk tiles t = warp id, + grid warps,
+// ... with those columns read from shared memory (LDS: a few bank wavefronts per warp instead of
+// one L2 sector per lane) and the rest gathered from the L2 as usual.
+template <bool HOT, bool SCATTER>
+__global__ void __launch_bounds__(kHotWarps * 32, 1) merge_hot_kernel(
+    const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
+    const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row, double* __restrict__ carry_val,
+    uint32_t tiles, const uint32_t* __restrict__ hot_cols, uint32_t nhot, const __grid_constant__ RowDest dest) {
+  extern __shared__ __align__(16) double s_hot[];
+  __shared__ __align__(16) uint16_t s_map_all[kHotWarps][256];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const uint64_t pl = policy_evict_last(), ps = policy_evict_first();
+  if constexpr (HOT) {
+    for (uint32_t i = threadIdx.x; i < nhot; i += kHotWarps * 32) s_hot[i] = ld_x(x + __ldg(hot_cols + i), pl);
+    __syncthreads();
+  }
+  for (uint32_t t = blockIdx.x * kHotWarps + warp; t < tiles; t += gridDim.x * kHotWarps)
+    merge_tile8<HOT, SCATTER>(row_ptr, col, val, x, s_hot, y, tile_row, tile_nnz, carry_row, carry_val, t,
+                              s_map_all[warp], lane, dest, pl, ps);
 }
 
 // ---------------------------------------------------------------- carry fix-up
@@ -447,6 +720,46 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
 
 // The tile kernels' own peer push (SCATTER) is used without panels; a panelled multiply pushes
 // all its rows after the last panel (push_all_rows).
+// The hot-x plan (one panel only): persistent merge_hot_kernel, then the carry fix-up.
+void launch_merge_hot(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
+                      const RowDest& dest) {
+  once_per_device([] {
+    cudaFuncSetAttribute(merge_hot_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMaxSlots * 8);
+    cudaFuncSetAttribute(merge_hot_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMaxSlots * 8);
+  });
+  const uint32_t tiles = f.merge_tiles;
+  const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
+  const uint32_t* col = f.find("merge_hot_col")->as<uint32_t>();
+  const double* val = f.find("data")->as<double>();
+  const uint32_t* hot = f.find("merge_hot_cols")->as<uint32_t>();
+  const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>();
+  const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>();
+  const unsigned grid = std::min<uint32_t>(kNumSMs, (tiles + kHotWarps - 1) / kHotWarps);
+  const size_t smem = (size_t)f.merge_hot * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kHotWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dest.n)
+    cudaLaunchKernelEx(&cfg, merge_hot_kernel<true, true>, rp, col, val, x, y, trow, tnnz, sc->carry_row, sc->carry_val,
+                       tiles, hot, f.merge_hot, dest);
+  else
+    cudaLaunchKernelEx(&cfg, merge_hot_kernel<true, false>, rp, col, val, x, y, trow, tnnz, sc->carry_row, sc->carry_val,
+                       tiles, hot, f.merge_hot, dest);
+  if (dest.n)
+    launch_pdl(merge_fixup_kernel<true, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
+               (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
+  else
+    launch_pdl(merge_fixup_kernel<false, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
+               (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
+}
+
 template <int IPT>
 void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
                       const RowDest& dest, uint32_t k) {
@@ -529,6 +842,13 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
   if (!sc) {
     g_last_error = "device allocation failed (merge carry scratch)";
     return kNoMemory;
+  }
+  if (f.merge_hot) {
+    timing_begin("merge_hot_kernel", s);
+    launch_merge_hot(f, x, y, sc, s, dest);
+    note_launch(2);
+    timing_end(s);
+    return check_launch("spmv_merge");
   }
   timing_begin("merge_spmv_vec_kernel", s);
   for (uint32_t k = 0; k < f.merge_panels; ++k) {

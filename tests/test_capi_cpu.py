@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), f"{n} declared in spmvlab_cuda.h but not exported"
     assert set(names) == set(capi.EXPORTS)
-    assert lib.spmvlab_cuda_abi_version() == 2
+    assert lib.spmvlab_cuda_abi_version() == 3
 
 
 def test_library_is_sm100a():

@@ -1,0 +1,174 @@
+"""GPU parity: the merge engine's hot-x plan (build_hot_columns + merge_hot_kernel).
+
+On a column-skewed matrix (R-MAT) the build gives the most referenced columns a shared-memory
+slot: the plan copy merge_hot_col of col_ind marks their entries 0x80000000 | slot and
+merge_hot_cols lists them; the persistent tile kernel reads those x values from shared memory.
+The plan arrays are checked bit for bit against a numpy restatement of the selection rule, and y
+against the oracle within the BASELINE tolerance -- over slot caps, tile counts, long and empty
+rows, the fused-exchange (scatter) epilogue and the iterated loop.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from parity import assert_y_close
+
+pytestmark = pytest.mark.gpu
+
+MERGE = 2
+MAX_SLOTS, MIN_REFS, MIN_SHARE = 12288, 32, 0.10
+
+
+def _hot_ref(n, nnz, crs_col, cap=MAX_SLOTS):
+    """The selection rule of build_hot_columns restated: per-column reference counts (clamped at
+    65535 for the threshold search); the threshold T is the smallest count >= MIN_REFS such that
+    the columns with count >= T fit in cap; kept when they cover MIN_SHARE of the entries."""
+    cnt = np.bincount(crs_col.astype(np.int64), minlength=n)
+    hist = np.bincount(np.minimum(cnt, 65535), minlength=65536)
+    take = refs = thr = 0
+    for c in range(65535, MIN_REFS - 1, -1):
+        if take + hist[c] > cap:
+            break
+        take += hist[c]
+        refs += c * hist[c]
+        if hist[c]:
+            thr = c
+    if thr == 0 or take == 0 or refs < MIN_SHARE * nnz:
+        return None
+    hot = np.nonzero(cnt >= thr)[0]
+    slot = np.full(n, -1, np.int64)
+    slot[hot] = np.arange(len(hot))
+    s = slot[crs_col.astype(np.int64)]
+    remap = np.where(s >= 0, s | 0x80000000, crs_col.astype(np.int64)).astype(np.uint32)
+    return hot.astype(np.uint32), remap, refs / nnz
+
+
+def _build(sp, monkeypatch, m, n, r, c, v, **env):
+    for k, val in env.items():
+        monkeypatch.setenv(k, str(val))
+    f = sp.build_format(MERGE, sp.TripletMatrix.from_host(m, n, r, c, v), 1)
+    for k in env:
+        monkeypatch.delenv(k)
+    return f
+
+
+def _check(sp, oracle, f, m, n, r, c, v, x, cap=MAX_SLOTS, what=""):
+    ref = oracle.build(0, m, n, r, c, v)
+    want = _hot_ref(n, len(v), ref.arrays["col_ind"], cap)
+    assert want is not None, "the matrix should get a hot-x plan"
+    hot, remap, share = want
+    assert f.info["merge_hot_slots"] == len(hot)
+    assert abs(f.info["merge_hot_share"] - share) < 1e-12
+    np.testing.assert_array_equal(f.array("merge_hot_cols"), hot)
+    np.testing.assert_array_equal(f.array("merge_hot_col"), remap)
+    np.testing.assert_array_equal(f.array("col_ind"), ref.arrays["col_ind"])  # storage untouched
+    y = sp.run_spmv(MERGE, f, torch.from_numpy(x).cuda(), p=1).cpu().numpy()
+    assert_y_close(y, oracle.spmv(ref, 0, x), oracle.abs_spmv(m, r, c, v, x), what=what)
+    return ref
+
+
+@pytest.mark.parametrize("scale,ef,cap,tiles", [(14, 16, None, None), (15, 8, None, None), (14, 16, 64, None),
+                                                (14, 16, 1000, 1), (16, 16, None, 16), (13, 4, None, 3)])
+def test_hot_rmat(cuda, oracle, monkeypatch, scale, ef, cap, tiles):
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(scale, ef, seed=scale + ef)
+    env = {}
+    if cap is not None:
+        env["SPMVLAB_MERGE_HOT_SLOTS"] = cap
+    if tiles is not None:
+        env["SPMVLAB_MERGE_HOT_TILES"] = tiles
+    f = _build(sp, monkeypatch, m, n, r, c, v, **env)
+    x = np.random.default_rng(scale).uniform(-1, 1, n)
+    _check(sp, oracle, f, m, n, r, c, v, x, cap or MAX_SLOTS, what=f"rmat s{scale} ef{ef} cap={cap} tiles={tiles}")
+    # without the plan the same format gives the same y within tolerance (and ParCRS / SeqCrs
+    # on it read the untouched col_ind)
+    f0 = _build(sp, monkeypatch, m, n, r, c, v, SPMVLAB_MERGE_HOT=0)
+    assert f0.info["merge_hot_slots"] == 0
+    ref = oracle.build(0, m, n, r, c, v)
+    xd = torch.from_numpy(x).cuda()
+    np.testing.assert_array_equal(sp.run_spmv(0, f, xd, p=1).cpu().numpy(), oracle.spmv(ref, 0, x))
+
+
+def test_hot_long_and_empty_rows(cuda, oracle, monkeypatch):
+    """Hot columns inside rows spanning many tiles, runs of empty rows, rows of one entry."""
+    sp = cuda
+    rng = np.random.default_rng(11)
+    m, n = 70000, 40000
+    hotc = rng.choice(n, 300, replace=False)
+    rows, cols = [], []
+    rows.append(np.full(30000, 5)); cols.append(rng.choice(n, 30000, replace=False))          # long row
+    rows.append(np.full(n, 69999)); cols.append(np.arange(n))                                  # full last row
+    rr = rng.integers(100, 20000, 60000)                                                       # rows >= 20000 stay empty
+    rows.append(rr); cols.append(np.where(rng.random(60000) < 0.7, rng.choice(hotc, 60000), rng.integers(0, n, 60000)))
+    rows.append(np.arange(40000, 40500)); cols.append(rng.choice(hotc, 500))                  # single-entry rows
+    r = np.concatenate(rows).astype(np.int64)
+    c = np.concatenate(cols).astype(np.int64)
+    key = np.unique(r * n + c)
+    r, c = (key // n).astype(np.uint32), (key % n).astype(np.uint32)
+    v = rng.uniform(-1, 1, len(key))
+    perm = rng.permutation(len(key))
+    r, c, v = r[perm], c[perm], v[perm]
+    for tiles in (1, 4, 64):
+        f = _build(sp, monkeypatch, m, n, r, c, v, SPMVLAB_MERGE_HOT_TILES=tiles)
+        for seed in (1, 2):
+            x = np.random.default_rng(seed).uniform(-1, 1, n)
+            _check(sp, oracle, f, m, n, r, c, v, x, what=f"tiles={tiles} seed={seed}")
+
+
+def test_hot_plan_skipped_without_skew(cuda, oracle, monkeypatch):
+    """Uniform columns (ER, mean degree 16): no column reaches the reference count, no plan."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.er_host(1 << 14, 16.0, seed=3)
+    f = _build(sp, monkeypatch, m, n, r, c, v)
+    assert f.info["merge_hot_slots"] == 0
+    assert _hot_ref(n, len(v), oracle.build(0, m, n, r, c, v).arrays["col_ind"]) is None
+
+
+def test_hot_scatter_epilogue(cuda, oracle, monkeypatch):
+    """spmvlab_cuda_run_spmv_scatter on a hot-x plan: y, and every destination buffer receives the
+    shard's rows at the row offset (the fused exchange's epilogue, here with local buffers)."""
+    from paper_2502_19284_b200 import capi, gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(14, 16, seed=9)
+    f = _build(sp, monkeypatch, m, n, r, c, v, SPMVLAB_MERGE_HOT_TILES=2)
+    assert f.info["merge_hot_slots"] > 0
+    ref = oracle.build(0, m, n, r, c, v)
+    x = np.random.default_rng(4).uniform(-1, 1, n)
+    y_ref = oracle.spmv(ref, 0, x)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full((m,), np.nan, dtype=torch.float64, device="cuda")
+    off, dlen = 1234, m + 5000
+    dests = [torch.full((dlen,), -7.0, dtype=torch.float64, device="cuda") for _ in range(3)]
+    arr = (C.c_void_p * 3)(*[d.data_ptr() for d in dests])
+    rc = capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, xd.data_ptr(), n, y.data_ptr(), m, arr, 3, dlen, off,
+                                                   torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, capi.load().spmvlab_cuda_last_error()
+    torch.cuda.synchronize()
+    bound = oracle.abs_spmv(m, r, c, v, x)
+    assert_y_close(y.cpu().numpy(), y_ref, bound, what="hot scatter y")
+    for d in dests:
+        dh = d.cpu().numpy()
+        np.testing.assert_array_equal(dh[off:off + m], y.cpu().numpy())
+        assert (dh[:off] == -7.0).all() and (dh[off + m:] == -7.0).all()
+
+
+def test_hot_iterate(cuda, oracle, monkeypatch):
+    """The iterated loop (x <- A x, normalised) over a hot-x plan vs the oracle loop."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(13, 16, seed=21, normalize_columns=True)
+    f = _build(sp, monkeypatch, m, n, r, c, v)
+    assert f.info["merge_hot_slots"] > 0
+    ref = oracle.build(0, m, n, r, c, v)
+    x = np.full(n, 1.0 / n)
+    xd = torch.from_numpy(x.copy()).cuda()
+    out = sp.iterate(MERGE, f, xd, 5, p=1)
+    xr = x.copy()
+    for _ in range(5):
+        xr = oracle.spmv(ref, 0, xr)
+    got = (out[0] if isinstance(out, tuple) else out).cpu().numpy()
+    np.testing.assert_allclose(got, xr, rtol=1e-11, atol=1e-300)
