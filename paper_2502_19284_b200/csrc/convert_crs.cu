@@ -372,9 +372,11 @@ int build_merge_plan(Format& f, Arena& ar) {
   }
   f.merge_hot = 0;
   f.merge_hot_share = 0.0;
+  f.merge_persist = false;
   if (panels == 1 && f.alg == kMerge) {
     if (int rc = build_hot_columns(f, ar)) return rc;
-    if (f.merge_hot) {
+    f.merge_persist = f.merge_hot > 0;
+    if (f.merge_persist) {
       // equal merge-path shares, kHotTilesPerWarp per warp of the persistent grid
       uint64_t per = (uint64_t)kNumSMs * kHotWarps * kHotTilesPerWarp;
       if (const char* e = getenv("SPMVLAB_MERGE_HOT_TILES")) per = (uint64_t)kNumSMs * kHotWarps * std::max(1, atoi(e));

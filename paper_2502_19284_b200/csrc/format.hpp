@@ -52,6 +52,7 @@ struct spmvlab_cuda_format {
   // hot-x plan (one panel only): merge_hot x entries copied to shared memory per SM; their column
   // indices in the plan copy "merge_hot_col" carry 0x80000000 | slot, "merge_hot_cols" lists them
   uint32_t merge_hot = 0;
+  bool merge_persist = false;    // persistent 8-wide tile kernel (always with a hot-x plan)
   double merge_hot_share = 0.0;  // share of the nonzeros whose x comes from the copy
 
   // ---- ParCRS launch shape

@@ -720,44 +720,37 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
 
 // The tile kernels' own peer push (SCATTER) is used without panels; a panelled multiply pushes
 // all its rows after the last panel (push_all_rows).
-// The hot-x plan (one panel only): persistent merge_hot_kernel, then the carry fix-up.
-void launch_merge_hot(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
-                      const RowDest& dest) {
-  once_per_device([] {
-    cudaFuncSetAttribute(merge_hot_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMaxSlots * 8);
-    cudaFuncSetAttribute(merge_hot_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMaxSlots * 8);
-  });
+// The persistent plan (one panel only; with or without hot x): merge_hot_kernel, then the carry fix-up.
+template <bool HOT, bool SCATTER>
+void launch_merge_persistent(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
+                             const RowDest& dest) {
+  if (HOT)
+    once_per_device([] {
+      cudaFuncSetAttribute(merge_hot_kernel<HOT, SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kHotMaxSlots * 8);
+    });
   const uint32_t tiles = f.merge_tiles;
   const uint32_t* rp = f.find("row_ptr")->as<uint32_t>();
-  const uint32_t* col = f.find("merge_hot_col")->as<uint32_t>();
+  const uint32_t* col = f.find(HOT ? "merge_hot_col" : "col_ind")->as<uint32_t>();
   const double* val = f.find("data")->as<double>();
-  const uint32_t* hot = f.find("merge_hot_cols")->as<uint32_t>();
+  const uint32_t* hot = HOT ? f.find("merge_hot_cols")->as<uint32_t>() : nullptr;
   const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>();
   const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>();
   const unsigned grid = std::min<uint32_t>(kNumSMs, (tiles + kHotWarps - 1) / kHotWarps);
-  const size_t smem = (size_t)f.merge_hot * 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kHotWarps * 32);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = HOT ? (size_t)f.merge_hot * 8 : 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (dest.n)
-    cudaLaunchKernelEx(&cfg, merge_hot_kernel<true, true>, rp, col, val, x, y, trow, tnnz, sc->carry_row, sc->carry_val,
-                       tiles, hot, f.merge_hot, dest);
-  else
-    cudaLaunchKernelEx(&cfg, merge_hot_kernel<true, false>, rp, col, val, x, y, trow, tnnz, sc->carry_row, sc->carry_val,
-                       tiles, hot, f.merge_hot, dest);
-  if (dest.n)
-    launch_pdl(merge_fixup_kernel<true, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
-               (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
-  else
-    launch_pdl(merge_fixup_kernel<false, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
-               (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
+  cudaLaunchKernelEx(&cfg, merge_hot_kernel<HOT, SCATTER>, rp, col, val, x, y, trow, tnnz, sc->carry_row,
+                     sc->carry_val, tiles, hot, HOT ? f.merge_hot : 0u, dest);
+  launch_pdl(merge_fixup_kernel<SCATTER, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
+             (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
 }
 
 template <int IPT>
@@ -843,9 +836,12 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
     g_last_error = "device allocation failed (merge carry scratch)";
     return kNoMemory;
   }
-  if (f.merge_hot) {
+  if (f.merge_persist) {
     timing_begin("merge_hot_kernel", s);
-    launch_merge_hot(f, x, y, sc, s, dest);
+    // (the same kernel without hot x -- x gathers only, more L1 for them -- measured slower than
+    // merge_spmv_vec_kernel: cfg2 307 vs 292 us, cfg3 unpanelled 1059 vs 998 us)
+    if (dest.n) launch_merge_persistent<true, true>(f, x, y, sc, s, dest);
+    else launch_merge_persistent<true, false>(f, x, y, sc, s, dest);
     note_launch(2);
     timing_end(s);
     return check_launch("spmv_merge");
