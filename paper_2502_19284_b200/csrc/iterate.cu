@@ -10,10 +10,11 @@
 // One pass per iteration after the multiply, with a deferred scale: the stored vector u_k and a
 // device scalar s_k with x_k = s_k u_k.  The engine multiplies the stored vector, y = A u_k, and
 // the pass reads y (and u_k for the residual) once: t = s_k y_r = (A x_k)_r is summed into the
-// mass, |t - s_k u_k[r]| into the residual, and (rescaling) t is written back, so the stored vector
-// is A x_k and s_{k+1} = 1 / mass_k.  The last iterate is scaled once at the end.  Traffic per row:
-// 24 B with rescale and norms, 16 B for either alone (two passes -- mass, then rescale -- were 32 B
-// and two launches); nothing at all when neither is asked for.
+// mass and |t - s_k u_k[r]| into the residual; rescaling keeps y as the stored vector and sets
+// s_{k+1} = s_k / mass_k (y is written back scaled only when s drifts out of [2^-256, 2^256]).  The
+// last iterate is scaled once at the end.  Traffic per row: 16 B with the residual, 8 B for the mass
+// alone (the write-back of every rescaled iterate was 24 B; two passes -- mass, then rescale --
+// were 32 B and two launches); nothing at all when neither norms nor rescaling are asked for.
 //
 // Folding the mass and the scale into the merge kernel itself (tile partial sums of the products,
 // every stored row scaled) measured SLOWER than this pass: the latency-bound merge kernel loses an
@@ -58,12 +59,16 @@ __global__ void init_scratch_kernel(IterScratch* sc) {
   sc->iter = 0;
 }
 
-// The pass after iteration k's multiply (see the file comment).  RESCALE: write t = s_k y back and
-// set s_{k+1} = 1 / mass; RESIDUAL: read u_k and accumulate |t - s_k u_k|.  Always: the mass.
+// The pass after iteration k's multiply (see the file comment).  RESIDUAL: read u_k and accumulate
+// |t - s_k u_k|.  Always: the mass.  RESCALE: x_{k+1} = A x_k / mass_k = (s_k / mass_k) y, so the
+// stored vector stays y and only the scalar changes, s_{k+1} = s_k / mass_k -- unless s_k has
+// drifted outside [2^-256, 2^256] (y itself then grows or shrinks with every iteration): then t is
+// written back and s_{k+1} = 1 / mass_k.  The test is uniform over the grid.
 template <bool RESCALE, bool RESIDUAL>
 __global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __restrict__ u, double* __restrict__ y,
                                                                 uint64_t n, IterScratch* sc, double* norms) {
   const double s = sc->scale;
+  const bool write_back = RESCALE && !(fabs(s) >= 0x1p-256 && fabs(s) <= 0x1p256);
   double d = 0.0, m = 0.0;
   const uint64_t n2 = n / 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __
         double2 t;
         t.x = one(yv[k].x, RESIDUAL ? uv[k].x : 0.0);
         t.y = one(yv[k].y, RESIDUAL ? uv[k].y : 0.0);
-        if (RESCALE) y2[i + k * stride] = t;
+        if (write_back) y2[i + k * stride] = t;
       }
     }
     for (; i < n2; i += stride) {
@@ -99,16 +104,16 @@ __global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __
       double2 t;
       t.x = one(yv.x, uv.x);
       t.y = one(yv.y, uv.y);
-      if (RESCALE) y2[i] = t;
+      if (write_back) y2[i] = t;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {  // the odd tail element
       const double t = one(y[n - 1], RESIDUAL ? u[n - 1] : 0.0);
-      if (RESCALE) y[n - 1] = t;
+      if (write_back) y[n - 1] = t;
     }
   } else {
     for (; i < n; i += stride) {
       const double t = one(y[i], RESIDUAL ? u[i] : 0.0);
-      if (RESCALE) y[i] = t;
+      if (write_back) y[i] = t;
     }
   }
   __shared__ double sd[kRedThreads / 32], sm[kRedThreads / 32];
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __
     double* out = iter_out(sc, norms);
     out[0] = RESIDUAL ? td : 0.0;
     out[1] = tm;
-    if (RESCALE) sc->scale = 1.0 / tm;
+    if (RESCALE) sc->scale = write_back ? 1.0 / tm : s / tm;
     sc->ticket = 0;  // ready for the next reduction (stream order)
     sc->iter += 1;
   }
