@@ -363,13 +363,15 @@ int spmvlab_cuda_iterate(int alg, const spmvlab_cuda_format* f, double* x, doubl
   auto mult = [&](const double* xi, double* yi, cudaStream_t st) {
     return spmvlab_cuda_run_spmv(alg, f, xi, f->n, yi, f->m, p, nullptr, st);
   };
-  if (!(flags & SPMVLAB_ITER_GRAPH) || iters == 0) return iterate(*f, mult, x, work, iters, flags, norms, s);
+  const bool merge_engine = alg == kMerge && is_crs_alg(f->alg);
+  if (!(flags & SPMVLAB_ITER_GRAPH) || iters == 0)
+    return iterate(*f, mult, x, work, iters, flags, norms, s, merge_engine);
   if (!s) return fail(kInvalidArgument, "graph mode needs a non-default stream");
   // nothing may allocate synchronously inside the capture: create this stream's carry scratch now
   if (alg == kMerge && is_crs_alg(f->alg) && !f->stream_scratch(s))
     return fail(kNoMemory, "device allocation failed (merge carry scratch)");
   const bool timing = timing_enable(false);  // no event brackets inside a capture
-  const int rc = iterate(*f, mult, x, work, iters, flags, norms, s);
+  const int rc = iterate(*f, mult, x, work, iters, flags, norms, s, merge_engine);
   timing_enable(timing);
   return rc;
 }

@@ -27,6 +27,7 @@
 // every iteration pair (x -> work -> x) are identical: graph mode captures ONE pair and replays it
 // iters / 2 times.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <utility>
 
@@ -38,16 +39,7 @@ extern thread_local std::string g_last_error;
 namespace {
 
 constexpr int kRedThreads = 256;
-constexpr unsigned kRedBlocks = 8 * kNumSMs;
 constexpr int kRedUnroll = 4;  // double2 per thread per step
-
-struct IterScratch {
-  double partial[2 * kRedBlocks];
-  double pair[2];    // (residual, mass) of the current iteration when the caller keeps no norms
-  double scale;      // s_k: x_k = scale * stored vector
-  unsigned ticket;   // CTAs finished in the current reduction
-  unsigned iter;     // iteration index (selects norms + 2 * iter)
-};
 
 __device__ __forceinline__ double* iter_out(IterScratch* sc, double* norms) {
   return norms ? norms + 2ull * sc->iter : sc->pair;
@@ -55,6 +47,7 @@ __device__ __forceinline__ double* iter_out(IterScratch* sc, double* norms) {
 
 __global__ void init_scratch_kernel(IterScratch* sc) {
   sc->scale = 1.0;
+  sc->pscale = 1.0;
   sc->ticket = 0;
   sc->iter = 0;
 }
@@ -67,6 +60,7 @@ __global__ void init_scratch_kernel(IterScratch* sc) {
 template <bool RESCALE, bool RESIDUAL>
 __global__ void __launch_bounds__(kRedThreads) iter_pass_kernel(const double* __restrict__ u, double* __restrict__ y,
                                                                 uint64_t n, IterScratch* sc, double* norms) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched behind the multiply (PDL)
   const double s = sc->scale;
   const bool write_back = RESCALE && !(fabs(s) >= 0x1p-256 && fabs(s) <= 0x1p256);
   double d = 0.0, m = 0.0;
@@ -175,12 +169,25 @@ template <bool RESCALE, bool RESIDUAL>
 void launch_pass(const double* u, double* y, uint64_t n, IterScratch* sc, double* norms, cudaStream_t s) {
   const uint64_t want = (n + 2ull * kRedThreads * kRedUnroll - 1) / (2ull * kRedThreads * kRedUnroll);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks, want));
-  iter_pass_kernel<RESCALE, RESIDUAL><<<grid, kRedThreads, 0, s>>>(u, y, n, sc, norms);
+  // programmatic dependent launch: the pass is resident while the multiply's fix-up drains
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRedThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, iter_pass_kernel<RESCALE, RESIDUAL>, u, y, n, sc, norms);
   note_launch();
 }
 
-int one_iteration(const SpmvFn& multiply, const double* cur, double* nxt, uint64_t n, bool normalize, double* norms,
-                  IterScratch* sc, cudaStream_t s) {
+int one_iteration(const Format& f, const SpmvFn& multiply, bool fused, const double* cur, double* nxt, uint64_t n,
+                  bool normalize, double* norms, IterScratch* sc, cudaStream_t s) {
+  // (the residual inside the multiply -- NORMS = 2 -- measured slower than this pass: cfg2 346 vs
+  // 302 us per iteration; the mass alone is free there: 280 vs 298 us)
+  if (fused && normalize && !norms) return spmv_merge_norms(f, cur, nxt, s, sc);
   if (int rc = multiply(cur, nxt, s)) return rc;
   if (normalize && norms) launch_pass<true, true>(cur, nxt, n, sc, norms, s);
   else if (normalize) launch_pass<true, false>(cur, nxt, n, sc, norms, s);
@@ -191,9 +198,13 @@ int one_iteration(const SpmvFn& multiply, const double* cur, double* nxt, uint64
 }  // namespace
 
 int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
-            double* norms, cudaStream_t s) {
+            double* norms, cudaStream_t s, bool merge_engine) {
   const uint64_t n = f.n;
   const bool normalize = flags & 1, graph = flags & 2;
+  // norms inside the multiply (hot-x plan of the merge engine); SPMVLAB_ITER_FUSED=0 (developer)
+  // keeps the separate pass
+  bool fused = merge_engine && merge_norms_supported(f);
+  if (const char* e = getenv("SPMVLAB_ITER_FUSED")) fused = fused && atoi(e) != 0;
   IterScratch* sc = nullptr;
   if (cudaMallocAsync(&sc, sizeof(IterScratch), s) != cudaSuccess) {
     cudaGetLastError();
@@ -213,8 +224,8 @@ int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, ui
     if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       rc = check_launch("iterate(capture)");
     } else {
-      rc = one_iteration(multiply, x, work, n, normalize, norms, sc, s);
-      if (rc == kOk) rc = one_iteration(multiply, work, x, n, normalize, norms, sc, s);
+      rc = one_iteration(f, multiply, fused, x, work, n, normalize, norms, sc, s);
+      if (rc == kOk) rc = one_iteration(f, multiply, fused, work, x, n, normalize, norms, sc, s);
       const cudaError_t ce = cudaStreamEndCapture(s, &g);
       if (rc == kOk && ce != cudaSuccess) rc = check_launch("iterate(capture)");
     }
@@ -232,7 +243,7 @@ int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, ui
   double* nxt = work;
   if (done & 1) std::swap(cur, nxt);
   for (; rc == kOk && done < iters; ++done) {
-    rc = one_iteration(multiply, cur, nxt, n, normalize, norms, sc, s);
+    rc = one_iteration(f, multiply, fused, cur, nxt, n, normalize, norms, sc, s);
     std::swap(cur, nxt);
   }
   if (rc == kOk && normalize && n) {  // x = s * stored vector (in place or into x)

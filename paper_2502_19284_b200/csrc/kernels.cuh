@@ -81,8 +81,27 @@ int spmv_blocked(const Format& f, const double* x, double* y, cudaStream_t s);
 
 // ---- iterated multiply (iterate.cu): x <- A x, `iters` times, with optional norms / rescaling
 using SpmvFn = std::function<int(const double* x, double* y, cudaStream_t s)>;
+// merge_engine: the multiply is the merge engine on this (CRS) format, so a hot-x plan may run the
+// loop's norms inside the multiply (spmv_merge_norms)
 int iterate(const Format& f, const SpmvFn& multiply, double* x, double* work, uint32_t iters, int flags,
-            double* norms, cudaStream_t s);
+            double* norms, cudaStream_t s, bool merge_engine = false);
+
+// Device state of the loop (iterate.cu; the fused merge epilogue in spmv_crs.cu updates it too).
+constexpr unsigned kRedBlocks = 8 * kNumSMs;
+struct IterScratch {
+  double partial[2 * kRedBlocks];
+  double pair[2];    // (residual, mass) of the current iteration when the caller keeps no norms
+  double scale;      // s_k: x_k = scale * stored vector
+  unsigned ticket;   // CTAs finished in the current reduction
+  unsigned iter;     // iteration index (selects norms + 2 * iter)
+  double cpart[kNumSMs];      // per-CTA mass of the fused merge kernel
+  double pscale;              // fused loop: factor on the next multiply's products (drift correction)
+};
+// One rescaled iteration without norms, y = A u with the mass fused into the merge engine's hot-x
+// plan (tile kernel: products summed per CTA; carry fix-up: its last block sums them in a fixed
+// order and updates the scale as iter_pass_kernel does).  kInvalidArgument without a hot-x plan.
+bool merge_norms_supported(const Format& f);
+int spmv_merge_norms(const Format& f, const double* u, double* y, cudaStream_t s, IterScratch* sc);
 
 // ---- primitives
 int merge_path_search(const uint32_t* a, uint64_t a_len, const uint32_t* b, uint64_t b_len, const uint64_t* diags,

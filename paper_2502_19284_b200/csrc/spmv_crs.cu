@@ -453,6 +453,15 @@ __device__ __forceinline__ void products8(const double* __restrict__ val, const 
 // for the multiply alone)
 __device__ __forceinline__ void st_y(double* y, uint32_t r, double v, uint64_t) { y[r] = v; }
 
+// The rescaled loop's mass inside the persistent kernel (spmv_merge_norms, NORMS): sum of y = sum of
+// the products, per lane; sigma = a factor on the products (the loop's drift correction, 1 unless
+// the stored vector's scale left [2^-256, 2^256]).  (The residual sum |y_r - u_r| in here too --
+// u_r fetched with the row window, shuffled to the lane that finalises the row -- measured slower
+// than the loop's separate pass: cfg2 346 vs 302 us per iteration.)
+struct TileNorms {
+  double mass, sigma;
+};
+
 template <bool SCATTER>
 __device__ __forceinline__ void row_ends8(const uint32_t* __restrict__ row_ptr, double* __restrict__ y,
                                           uint16_t* smap, uint32_t r0, uint32_t base, uint32_t pend, uint32_t j0,
@@ -517,14 +526,15 @@ __device__ __forceinline__ void reduce8(double* __restrict__ y, const uint16_t* 
   __syncwarp();
 }
 
-template <bool HOT, bool SCATTER>
+template <bool HOT, bool SCATTER, bool NORMS>
 __device__ __forceinline__ void merge_tile8(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
                                             const double* __restrict__ val, const double* __restrict__ x,
                                             const double* sx, double* __restrict__ y,
                                             const uint32_t* __restrict__ tile_row,
                                             const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
                                             double* __restrict__ carry_val, uint32_t t, uint16_t* smap,
-                                            unsigned lane, const RowDest& dest, uint64_t pl, uint64_t ps) {
+                                            unsigned lane, const RowDest& dest, uint64_t pl, uint64_t ps,
+                                            TileNorms& nm) {
   *reinterpret_cast<uint4*>(smap + 8 * lane) = make_uint4(0u, 0u, 0u, 0u);
   const uint32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const uint32_t j0 = tile_nnz[t], j1 = tile_nnz[t + 1];
@@ -540,6 +550,11 @@ __device__ __forceinline__ void merge_tile8(const uint32_t* __restrict__ row_ptr
     double p[8];
     products8<HOT>(val, x, sx, cn, base + 8 * lane, j0, j1, pl, p);
     cn = cols8(col, base + 256u + 8 * lane, j0, j1);
+    if constexpr (NORMS) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) p[u] *= nm.sigma;
+      nm.mass += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+    }
     const uint32_t rp0 = rp;
     row_ends8<SCATTER>(row_ptr, y, smap, r0, base, min(base + 256u, j1), j0, r1, rp, prevE, wb, wE, wS0, lane, ps);
     reduce8(y, smap, r0, rp0, p, carry, lane, ps);
@@ -582,12 +597,13 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
 // most referenced ones) into shared memory; its warps then walk tiles t = warp id, + grid warps,
 // ... with those columns read from shared memory (LDS: a few bank wavefronts per warp instead of
 // one L2 sector per lane) and the rest gathered from the L2 as usual.
-template <bool HOT, bool SCATTER>
+template <bool HOT, bool SCATTER, bool NORMS = false>
 __global__ void __launch_bounds__(kHotWarps * 32, 1) merge_hot_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, double* __restrict__ y, const uint32_t* __restrict__ tile_row,
     const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row, double* __restrict__ carry_val,
-    uint32_t tiles, const uint32_t* __restrict__ hot_cols, uint32_t nhot, const __grid_constant__ RowDest dest) {
+    uint32_t tiles, const uint32_t* __restrict__ hot_cols, uint32_t nhot, const __grid_constant__ RowDest dest,
+    double* __restrict__ cpart, const double* __restrict__ sigma) {
   extern __shared__ __align__(16) double s_hot[];
   __shared__ __align__(16) uint16_t s_map_all[kHotWarps][256];
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -598,9 +614,22 @@ __global__ void __launch_bounds__(kHotWarps * 32, 1) merge_hot_kernel(
     for (uint32_t i = threadIdx.x; i < nhot; i += kHotWarps * 32) s_hot[i] = ld_x(x + __ldg(hot_cols + i), pl);
     __syncthreads();
   }
+  TileNorms nm{0.0, NORMS ? *sigma : 1.0};
   for (uint32_t t = blockIdx.x * kHotWarps + warp; t < tiles; t += gridDim.x * kHotWarps)
-    merge_tile8<HOT, SCATTER>(row_ptr, col, val, x, s_hot, y, tile_row, tile_nnz, carry_row, carry_val, t,
-                              s_map_all[warp], lane, dest, pl, ps);
+    merge_tile8<HOT, SCATTER, NORMS>(row_ptr, col, val, x, s_hot, y, tile_row, tile_nnz, carry_row, carry_val, t,
+                                     s_map_all[warp], lane, dest, pl, ps, nm);
+  if constexpr (NORMS) {  // this CTA's mass: lanes by xor tree, then warps in order
+    __shared__ double s_m[kHotWarps];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nm.mass += __shfl_xor_sync(0xFFFFFFFFu, nm.mass, off);
+    if (lane == 0) s_m[warp] = nm.mass;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < kHotWarps; ++w) b += s_m[w];
+      cpart[blockIdx.x] = b;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- carry fix-up
@@ -612,13 +641,10 @@ __global__ void __launch_bounds__(kHotWarps * 32, 1) merge_hot_kernel(
 // Deterministic (fixed reduction order) and O(run / 32) dependent steps for the longest rows.
 // (rows: the panel's compressed row ids, or null; m: the panel's row count)
 template <bool SCATTER, bool LAST>
-__global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
-                                   const double* __restrict__ carry_val, uint32_t tiles,
-                                   double* __restrict__ y, uint32_t m, const uint32_t* __restrict__ rows,
-                                   const __grid_constant__ RowDest dest) {
+__device__ __forceinline__ void fixup_runs(const uint32_t* __restrict__ carry_row, const double* __restrict__ carry_val,
+                                           uint32_t tiles, double* __restrict__ y, uint32_t m,
+                                           const uint32_t* __restrict__ rows, const RowDest& dest) {
   const unsigned lane = threadIdx.x & 31u;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u;
   if (base >= tiles) return;
   const uint32_t t = base + lane;
@@ -659,6 +685,56 @@ __global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
   if (lane == 0) {
     const uint32_t g = rows ? rows[r31] : r31;
     put_row<SCATTER, LAST>(y, dest, g, y[g] + total);
+  }
+}
+
+template <bool SCATTER, bool LAST>
+__global__ void merge_fixup_kernel(const uint32_t* __restrict__ carry_row,
+                                   const double* __restrict__ carry_val, uint32_t tiles,
+                                   double* __restrict__ y, uint32_t m, const uint32_t* __restrict__ rows,
+                                   const __grid_constant__ RowDest dest) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  fixup_runs<SCATTER, LAST>(carry_row, carry_val, tiles, y, m, rows, dest);
+}
+
+// The carry fix-up of spmv_merge_norms: merge_fixup_kernel's work (no peers, final y), then the
+// last block to finish (ticket) sums the tile kernel's per-CTA masses in a fixed order and updates
+// the loop state as iter_pass_kernel does for a rescaled iteration without norms (iterate.cu).
+__global__ void __launch_bounds__(256) merge_fixup_norms_kernel(const uint32_t* __restrict__ carry_row,
+                                                                const double* __restrict__ carry_val, uint32_t tiles,
+                                                                double* __restrict__ y, uint32_t m, IterScratch* sc,
+                                                                uint32_t nparts) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  fixup_runs<false, true>(carry_row, carry_val, tiles, y, m, nullptr, RowDest{});
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  __threadfence();
+  const unsigned lane = threadIdx.x;
+  double tm = 0.0;
+  for (uint32_t i = lane; i < nparts; i += 32) tm += __ldcg(sc->cpart + i);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tm += __shfl_xor_sync(0xFFFFFFFFu, tm, off);
+  if (lane == 0) {
+    // y = sigma A u_k and x_k = s_k u_k: mass_k = sum A x_k = (s_k / sigma) sum y; x_{k+1} = A x_k /
+    // mass_k = y / sum y, so the stored vector stays y and s_{k+1} = 1 / sum y -- if that leaves
+    // [2^-256, 2^256] the next multiply scales its products by it (sigma), which brings the next
+    // stored vector back to unit scale
+    const double sigma = sc->pscale, sk = sc->scale;
+    sc->pair[0] = 0.0;
+    sc->pair[1] = sk / sigma * tm;
+    const double nxt = 1.0 / tm;
+    sc->scale = nxt;
+    sc->pscale = (fabs(nxt) >= 0x1p-256 && fabs(nxt) <= 0x1p256) ? 1.0 : nxt;
+    sc->ticket = 0;
+    sc->iter += 1;
   }
 }
 
@@ -748,7 +824,8 @@ void launch_merge_persistent(const Format& f, const double* x, double* y, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, merge_hot_kernel<HOT, SCATTER>, rp, col, val, x, y, trow, tnnz, sc->carry_row,
-                     sc->carry_val, tiles, hot, HOT ? f.merge_hot : 0u, dest);
+                     sc->carry_val, tiles, hot, HOT ? f.merge_hot : 0u, dest, (double*)nullptr,
+                     (const double*)nullptr);
   launch_pdl(merge_fixup_kernel<SCATTER, true>, (tiles + 255) / 256, 256, s, sc->carry_row,
              (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
 }
@@ -774,6 +851,45 @@ void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch
 }
 
 }  // namespace
+
+bool merge_norms_supported(const Format& f) { return f.merge_persist && f.merge_hot && f.m == f.n; }
+
+int spmv_merge_norms(const Format& f, const double* u, double* y, cudaStream_t s, IterScratch* sc) {
+  if (!merge_norms_supported(f)) return kInvalidArgument;
+  const Scratch* cs = f.stream_scratch(s);
+  if (!cs) {
+    g_last_error = "device allocation failed (merge carry scratch)";
+    return kNoMemory;
+  }
+  once_per_device([] {
+    cudaFuncSetAttribute(merge_hot_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kHotMaxSlots * 8);
+  });
+  const uint32_t tiles = f.merge_tiles;
+  const unsigned grid = std::min<uint32_t>(kNumSMs, (tiles + kHotWarps - 1) / kHotWarps);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kHotWarps * 32);
+  cfg.dynamicSmemBytes = (size_t)f.merge_hot * 8;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  timing_begin("merge_hot_kernel", s);
+  cudaLaunchKernelEx(&cfg, merge_hot_kernel<true, false, true>, f.find("row_ptr")->as<uint32_t>(),
+                     (const uint32_t*)f.find("merge_hot_col")->as<uint32_t>(), (const double*)f.find("data")->as<double>(),
+                     u, y, (const uint32_t*)f.find("merge_tile_row")->as<uint32_t>(),
+                     (const uint32_t*)f.find("merge_tile_nnz")->as<uint32_t>(), cs->carry_row, cs->carry_val, tiles,
+                     (const uint32_t*)f.find("merge_hot_cols")->as<uint32_t>(), f.merge_hot, RowDest{}, sc->cpart,
+                     (const double*)&sc->pscale);
+  launch_pdl(merge_fixup_norms_kernel, (tiles + 255) / 256, 256, s, (const uint32_t*)cs->carry_row,
+             (const double*)cs->carry_val, tiles, y, f.m, sc, grid);
+  note_launch(2);
+  timing_end(s);
+  return check_launch("spmv_merge_norms");
+}
 
 int spmv_seq_crs(const Format& f, const double* x, double* y, cudaStream_t s) {
   if (f.m == 0) return kOk;

@@ -172,3 +172,74 @@ def test_hot_iterate(cuda, oracle, monkeypatch):
         xr = oracle.spmv(ref, 0, xr)
     got = (out[0] if isinstance(out, tuple) else out).cpu().numpy()
     np.testing.assert_allclose(got, xr, rtol=1e-11, atol=1e-300)
+
+
+def _oracle_loop(oracle, ref, x0, iters, normalize):
+    x, norms = x0.copy(), []
+    for _ in range(iters):
+        y = oracle.spmv(ref, 0, x)
+        mass = y.sum()
+        norms.append((np.abs(y - x).sum(), mass))
+        x = y / mass if normalize else y
+    return x, np.array(norms)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_hot_fused_rescaled_loop(cuda, oracle, monkeypatch, graph):
+    """A rescaled loop without norms runs the mass inside the hot-x multiply (per-CTA product sums,
+    the scale updated by the carry fix-up's last block): iterates against the oracle loop and
+    against the separate pass (SPMVLAB_ITER_FUSED=0); with norms kept, the loop's pass."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(14, 16, seed=33, normalize_columns=True)
+    f = _build(sp, monkeypatch, m, n, r, c, v, SPMVLAB_MERGE_HOT_TILES=3)
+    assert f.info["merge_hot_slots"] > 0
+    ref = oracle.build(0, m, n, r, c, v)
+    x0 = np.random.default_rng(8).uniform(0.0, 1.0, n) + 1e-3
+    x0 /= x0.sum()
+    want_x, want = _oracle_loop(oracle, ref, x0, 9, True)
+    res = {}
+    for fused in ("1", "0"):
+        for norms in (False, True):
+            monkeypatch.setenv("SPMVLAB_ITER_FUSED", fused)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                x = torch.from_numpy(x0.copy()).cuda()
+                _, nb = sp.iterate(MERGE, f, x, 9, normalize=True, norms=norms, graph=graph, stream=st)
+            st.synchronize()
+            monkeypatch.delenv("SPMVLAB_ITER_FUSED")
+            got = x.cpu().numpy()
+            np.testing.assert_allclose(got, want_x, rtol=2e-11, atol=1e-300)
+            assert abs(got.sum() - 1.0) < 1e-12
+            if norms:
+                nb = nb.cpu().numpy()
+                np.testing.assert_allclose(nb[:, 1], want[:, 1], rtol=1e-11)
+                np.testing.assert_allclose(nb[:, 0], want[:, 0], rtol=1e-9)
+            res[fused, norms] = got
+    np.testing.assert_allclose(res["1", False], res["0", False], rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_loop_scale_drift(cuda, oracle, monkeypatch, fused):
+    """Rescaling keeps the stored vector unscaled; when the scale leaves [2^-256, 2^256] (a matrix
+    whose iterates grow ~1e8 per step) the stored vector is written back scaled.  Both loop forms
+    against the oracle's normalised loop over 40 iterations."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(13, 16, seed=5)
+    v = v * 1e7
+    f = _build(sp, monkeypatch, m, n, r, c, v)
+    assert f.info["merge_hot_slots"] > 0
+    ref = oracle.build(0, m, n, r, c, v)
+    x0 = np.random.default_rng(9).uniform(0.0, 1.0, n) + 1e-3
+    x0 /= x0.sum()
+    want_x, want = _oracle_loop(oracle, ref, x0, 40, True)
+    monkeypatch.setenv("SPMVLAB_ITER_FUSED", fused)
+    x = torch.from_numpy(x0.copy()).cuda()
+    _, nb = sp.iterate(MERGE, f, x, 40, normalize=True, norms=fused == "0")  # no norms: the fused path
+    monkeypatch.delenv("SPMVLAB_ITER_FUSED")
+    got = x.cpu().numpy()
+    assert np.isfinite(got).all()
+    np.testing.assert_allclose(got, want_x, rtol=1e-10, atol=1e-300)
+    if nb is not None:
+        np.testing.assert_allclose(nb.cpu().numpy()[:, 1], want[:, 1], rtol=1e-10)

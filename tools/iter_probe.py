@@ -50,10 +50,10 @@ base = t_spmv()
 print(f"{name}: spmv {base*1e3:.1f} us  panels {f.info['merge_panels']}", flush=True)
 for unf in (False, True):
     if unf:
-        os.environ["SPMVLAB_ITER_UNFUSED"] = "1"
+        os.environ["SPMVLAB_ITER_FUSED"] = "0"
     for normalize, norms in ((False, False), (False, True), (True, False), (True, True)):
         for graph in (False, True):
             t = t_iter(normalize, norms, graph)
             print(f"  {'unfused' if unf else 'fused  '} normalize={normalize:d} norms={norms:d} graph={graph:d}: "
                   f"{t*1e3:8.1f} us/iter  ({t/base:.3f}x spmv)", flush=True)
-    os.environ.pop("SPMVLAB_ITER_UNFUSED", None)
+    os.environ.pop("SPMVLAB_ITER_FUSED", None)
