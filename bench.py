@@ -565,8 +565,19 @@ def main():
             t1.record(side)
             t1.synchronize()
             res["graph" if graph else "stream"] = t0.elapsed_time(t1) / iters
+        # the same loop keeping no norms (a rescaled loop then runs its mass inside the multiply)
+        side.wait_stream(stream)
+        xi = x.clone()
+        sp.iterate(sp.Algorithm.Merge, fmt, xi, 3, normalize=normalize, norms=False, work=work, stream=side)
+        side.synchronize()
+        t0.record(side)
+        sp.iterate(sp.Algorithm.Merge, fmt, xi, iters, normalize=normalize, norms=False, work=work, stream=side)
+        t1.record(side)
+        t1.synchronize()
+        res["stream_no_norms"] = t0.elapsed_time(t1) / iters
         iterate = {"engine": "merge", "iterations": iters, "normalize": normalize,
                    "ms_per_iteration": res, "spmv_ms": ms_step,
+                   "ratio_to_spmv": {k: t / ms_step for k, t in res.items()},
                    "final_diff_l1": float(nb[-1, 0]), "final_mass": float(nb[-1, 1])}
         del work
 

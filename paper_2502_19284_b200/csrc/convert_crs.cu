@@ -454,14 +454,26 @@ int build_merge_plan(Format& f, Arena& ar) {
 }
 
 // ---- hot-x plan of the merge engine (B200 design, no reference counterpart: a power-law column
-// distribution -- R-MAT -- sends a large share of the x gathers to few columns).  Columns
-// referenced at least T times, T the smallest count (>= kHotMinRefs) that keeps them within
-// kHotMaxSlots, get a shared-memory slot in column order; the plan copy merge_hot_col of col_ind
-// marks their entries 0x80000000 | slot.  Kept only when they cover kHotMinShare of the entries.
+// distribution -- R-MAT -- sends a large share of the x gathers to few columns).  Per-column
+// reference counts are taken over a sample of col_ind -- every kHotSample-th run of 32 consecutive
+// entries (all entries below 2^24 nonzeros) -- and scaled by the sampling stride.  Columns whose
+// count is at least T, T the smallest count (>= kHotMinRefs) that keeps them within kHotMaxSlots,
+// get a shared-memory slot in column order; the plan copy merge_hot_col of col_ind marks their
+// entries 0x80000000 | slot.  Kept only when they cover kHotMinShare of the (sampled) entries.
+// (Counting every entry took 0.75 ms at cfg2 -- 65 M atomics, most on a few hot columns.)
+constexpr uint32_t kHotSample = 8;
+constexpr uint64_t kHotSampleFrom = 1ull << 24;
+
 namespace {
-__global__ void col_ref_counts(const uint32_t* __restrict__ col, uint64_t nnz, uint32_t* __restrict__ cnt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) atomicAdd(cnt + col[k], 1u);
+__global__ void col_ref_counts(const uint32_t* __restrict__ col, uint64_t nnz, uint32_t stride_runs,
+                               uint32_t* __restrict__ cnt) {
+  const uint64_t runs = (nnz + 31) / 32;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * stride_runs < runs; w += nw) {
+    const uint64_t k = w * stride_runs * 32 + lane;
+    if (k < nnz) atomicAdd(cnt + col[k], 1u);
+  }
 }
 
 constexpr uint32_t kRefBins = 65536;  // counts clamped to kRefBins - 1
@@ -486,19 +498,20 @@ __global__ void hot_flags(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t
   if (i < n) flag[i] = cnt[i] >= thr;
 }
 
+// hot column list, and colmap[c] = the plan's index of column c (0x80000000 | slot, or c)
 __global__ void hot_fill(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t thr, const uint32_t* __restrict__ slot,
-                         uint32_t* __restrict__ hot_cols) {
+                         uint32_t* __restrict__ hot_cols, uint32_t* __restrict__ colmap) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && cnt[i] >= thr) hot_cols[slot[i]] = i;
+  if (i >= n) return;
+  const bool hot = cnt[i] >= thr;
+  if (hot) hot_cols[slot[i]] = i;
+  colmap[i] = hot ? (0x80000000u | slot[i]) : i;
 }
 
-__global__ void hot_remap(const uint32_t* __restrict__ col, uint64_t nnz, const uint32_t* __restrict__ cnt,
-                          uint32_t thr, const uint32_t* __restrict__ slot, uint32_t* __restrict__ out) {
+__global__ void hot_remap(const uint32_t* __restrict__ col, uint64_t nnz, const uint32_t* __restrict__ colmap,
+                          uint32_t* __restrict__ out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
-    const uint32_t c = col[k];
-    out[k] = cnt[c] >= thr ? (0x80000000u | slot[c]) : c;
-  }
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) out[k] = colmap[col[k]];
 }
 }  // namespace
 
@@ -515,24 +528,27 @@ int build_hot_columns(Format& f, Arena& ar) {
   if (!cnt || !hist) return kNoMemory;
   cudaMemsetAsync(cnt, 0, 4ull * f.n, s);
   cudaMemsetAsync(hist, 0, 4ull * kRefBins, s);
-  col_ref_counts<<<grid_for(f.nnz, 256), 256, 0, s>>>(col, f.nnz, cnt);
+  const uint32_t samp = f.nnz >= kHotSampleFrom ? kHotSample : 1u;
+  col_ref_counts<<<grid_for((f.nnz + samp - 1) / samp, 256), 256, 0, s>>>(col, f.nnz, samp, cnt);
   ref_count_hist<<<grid_for(f.n, 256, kNumSMs * 4), 256, 0, s>>>(cnt, f.n, hist);
   std::vector<uint32_t> h(kRefBins);
   cudaMemcpyAsync(h.data(), hist, 4ull * kRefBins, cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_hot_columns");
   uint64_t take = 0, refs = 0;
   uint32_t thr = 0;
-  for (uint32_t c = kRefBins - 1; c >= kHotMinRefs; --c) {
+  const uint32_t min_cnt = (kHotMinRefs + samp - 1) / samp;  // counts are of the sample
+  for (uint32_t c = kRefBins - 1; c >= min_cnt; --c) {
     if (take + h[c] > cap) break;
     take += h[c];
-    refs += (uint64_t)c * h[c];
+    refs += (uint64_t)c * h[c] * samp;
     if (h[c]) thr = c;
   }
   if (thr == 0 || take == 0 || (double)refs < kHotMinShare * (double)f.nnz) return check_launch("build_hot_columns");
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)f.n + 1);
+  uint32_t* colmap = ar.alloc_n<uint32_t>((uint64_t)f.n);
   uint32_t* hc = static_cast<uint32_t*>(f.add("merge_hot_col", f.nnz, 4, s));
   uint32_t* hl = static_cast<uint32_t*>(f.add("merge_hot_cols", take, 4, s));
-  if (!flag || !hc || !hl) {  // the hot-x plan is an optimisation: build without it
+  if (!flag || !colmap || !hc || !hl) {  // the hot-x plan is an optimisation: build without it
     cudaGetLastError();
     f.drop("merge_hot_col");
     f.drop("merge_hot_cols");
@@ -540,8 +556,8 @@ int build_hot_columns(Format& f, Arena& ar) {
   }
   hot_flags<<<grid_for(f.n, 256, 1u << 30), 256, 0, s>>>(cnt, f.n, thr, flag);
   exclusive_scan_u32(flag, flag, f.n, ar);
-  hot_fill<<<grid_for(f.n, 256, 1u << 30), 256, 0, s>>>(cnt, f.n, thr, flag, hl);
-  hot_remap<<<grid_for(f.nnz, 256), 256, 0, s>>>(col, f.nnz, cnt, thr, flag, hc);
+  hot_fill<<<grid_for(f.n, 256, 1u << 30), 256, 0, s>>>(cnt, f.n, thr, flag, hl, colmap);
+  hot_remap<<<grid_for(f.nnz, 256), 256, 0, s>>>(col, f.nnz, colmap, hc);
   uint32_t total = 0;
   cudaMemcpyAsync(&total, flag + f.n, 4, cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_hot_columns");

@@ -122,3 +122,20 @@ def test_cfg2_pinned_to_reference(cuda, reference, cfg2, alg):
         np.testing.assert_array_equal(y0, reference.spmv(ref0, 0, x, p=1))
     del f
     torch.cuda.empty_cache()
+
+
+def test_merge_hot_plan_full_size(cuda, cfg2):
+    """The merge engine's hot-x plan at full size (the sampled reference counts of 65.2M entries):
+    merge_hot_cols / merge_hot_col bit-exact against the numpy restatement of the selection rule
+    (tests/test_gpu_merge_hot.py), and the plan is in use (R-MAT's column skew)."""
+    from test_gpu_merge_hot import _hot_ref
+    sp = cuda
+    m, n, r, c, v = cfg2
+    f = sp.build_format(2, sp.TripletMatrix(m, n, r, c, v), 1)
+    col = f.array("col_ind")
+    want = _hot_ref(n, len(col), col)
+    assert want is not None and f.info["merge_hot_slots"] == len(want[0]) > 0
+    np.testing.assert_array_equal(f.array("merge_hot_cols"), want[0])
+    np.testing.assert_array_equal(f.array("merge_hot_col"), want[1])
+    assert abs(f.info["merge_hot_share"] - want[2]) < 1e-12
+    assert f.info["merge_hot_share"] > 0.3

@@ -21,18 +21,26 @@ MERGE = 2
 MAX_SLOTS, MIN_REFS, MIN_SHARE = 12288, 32, 0.10
 
 
+SAMPLE, SAMPLE_FROM = 8, 1 << 24
+
+
 def _hot_ref(n, nnz, crs_col, cap=MAX_SLOTS):
-    """The selection rule of build_hot_columns restated: per-column reference counts (clamped at
-    65535 for the threshold search); the threshold T is the smallest count >= MIN_REFS such that
-    the columns with count >= T fit in cap; kept when they cover MIN_SHARE of the entries."""
-    cnt = np.bincount(crs_col.astype(np.int64), minlength=n)
+    """The selection rule of build_hot_columns restated: per-column reference counts over the
+    sample (every SAMPLE-th run of 32 consecutive col_ind entries from 2^24 nonzeros on, all
+    entries below), clamped at 65535 for the threshold search; the threshold T is the smallest
+    sampled count >= ceil(MIN_REFS / stride) such that the columns with count >= T fit in cap; kept
+    when they cover MIN_SHARE of the entries (sampled counts times the stride)."""
+    samp = SAMPLE if nnz >= SAMPLE_FROM else 1
+    k = np.arange(nnz)
+    sampled = crs_col[(k >> 5) % samp == 0]
+    cnt = np.bincount(sampled.astype(np.int64), minlength=n)
     hist = np.bincount(np.minimum(cnt, 65535), minlength=65536)
     take = refs = thr = 0
-    for c in range(65535, MIN_REFS - 1, -1):
+    for c in range(65535, (MIN_REFS + samp - 1) // samp - 1, -1):
         if take + hist[c] > cap:
             break
         take += hist[c]
-        refs += c * hist[c]
+        refs += c * hist[c] * samp
         if hist[c]:
             thr = c
     if thr == 0 or take == 0 or refs < MIN_SHARE * nnz:
