@@ -138,8 +138,11 @@ def l2_roofline(cfg: int, kernel: str, kernel_ms: float):
         return None
     achieved = e["l2_to_sm_bytes_per_launch"] / (kernel_ms / 1e3) / 1e9
     peak = probe["l2_to_sm_bytes_per_launch"] / (probe["us"] / 1e6) / 1e9
-    return {"bytes_per_launch": e["l2_to_sm_bytes_per_launch"], "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "peak_kind": "probe (x-gather only kernel)"}
+    out = {"bytes_per_launch": e["l2_to_sm_bytes_per_launch"], "achieved": achieved, "peak": peak,
+           "unit": "GB/s", "frac": achieved / peak, "peak_kind": "probe (x-gather only kernel)"}
+    if "l1tex_lsu_wavefront_pct_of_peak" in e:  # the L1TEX data pipe (one wavefront per gathered line)
+        out["l1tex_data_pipe_pct_of_peak_ncu"] = e["l1tex_lsu_wavefront_pct_of_peak"]
+    return out
 
 
 def ev_time(fn, reps: int, warmup: int, stream) -> list:

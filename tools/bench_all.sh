@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end measurement set (run under gpurun): bench.py on every BASELINE config, the reference
 # arm, and the launch list of the default run.
-O=gpurun_out/bench_r02
+O=gpurun_out/bench_r02b
 mkdir -p $O
 python bench.py > $O/cfg2.json 2> $O/cfg2.err
 for c in 1 3 4; do python bench.py --config $c --steps 200 > $O/cfg$c.json 2> $O/cfg$c.err; done
