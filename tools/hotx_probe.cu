@@ -6,7 +6,9 @@
 //          x values copied into shared memory once per CTA; the rest by LDG
 #include <cstdint>
 #include <cstdio>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint64_t pol_first() {
   uint64_t p;
@@ -122,5 +124,81 @@ extern "C" int hp_run(int hot, int contig, int shape, const uint32_t* col, const
   S(0, 8, 6, 0) S(0, 24, 2, 1) S(0, 32, 1, 2) S(0, 16, 3, 3) S(0, 16, 2, 4)
   S(1, 8, 6, 0) S(1, 24, 2, 1) S(1, 32, 1, 2) S(1, 16, 3, 3) S(1, 16, 2, 4)
 #undef S
+  return -1;
+}
+
+// ---- cluster variant: a cluster of CL CTAs shares one hot copy of CL * Hl slots in distributed
+// shared memory; slot s lives in CTA (s % CL) at local index s / CL (remote reads through mapa)
+template <int CL>
+__device__ __forceinline__ double gxc(const double* __restrict__ x, double* const* peers, uint32_t c, uint64_t pl) {
+  double v;
+  if ((int)c < 0) {
+    const uint32_t s = c & 0x7FFFFFFFu;
+    v = peers[s % CL][s / CL];
+  } else {
+    v = ldx(x + c, pl);
+  }
+  return v;
+}
+
+template <int CL>
+__global__ void __launch_bounds__(1024, 1) k_cluster(const uint32_t* __restrict__ col, const double* __restrict__ val,
+                                                     uint64_t passes, const double* __restrict__ x,
+                                                     const double* __restrict__ xh, uint32_t H, double* out,
+                                                     int contig) {
+  extern __shared__ __align__(16) double sx[];
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  const uint32_t Hl = (H + CL - 1) / CL;
+  for (uint32_t i = threadIdx.x; i < Hl; i += blockDim.x) {
+    const uint32_t s = i * CL + rank;
+    sx[i] = s < H ? xh[s] : 0.0;
+  }
+  double* peers[CL];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) peers[r] = cl.map_shared_rank(sx, r);
+  cl.sync();
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t pf = pol_first(), pl = pol_last();
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0;
+  const uint64_t lo = contig ? w0 * passes / nw : w0, hi = contig ? (w0 + 1) * passes / nw : passes;
+  const uint64_t step = contig ? 1 : nw;
+  for (uint64_t q = lo; q < hi; q += step) {
+    const uint64_t k = q * 128 + 4 * lane;
+    const uint4 c = ld4(col + k, pf);
+    double v[4];
+    ldv4(val + k, pf, v);
+    acc += v[0] * gxc<CL>(x, peers, c.x, pl) + v[1] * gxc<CL>(x, peers, c.y, pl) + v[2] * gxc<CL>(x, peers, c.z, pl) +
+           v[3] * gxc<CL>(x, peers, c.w, pl);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
+  if (lane == 0) atomicAdd(out, acc);
+  cl.sync();  // peers' shared memory must outlive every remote read
+}
+
+extern "C" int hp_cluster(int CL, int contig, const uint32_t* col, const double* val, uint64_t passes, const double* x,
+                          const double* xh, uint32_t H, double* out, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148 / CL * CL);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = (size_t)((H + CL - 1) / CL) * 8;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define CLU(n)                                                                                                   \
+  if (CL == n) {                                                                                                 \
+    cudaFuncSetAttribute(k_cluster<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes); \
+    cudaLaunchKernelEx(&cfg, k_cluster<n>, col, val, passes, x, xh, H, out, contig);                            \
+    return (int)cudaGetLastError();                                                                              \
+  }
+  CLU(1) CLU(2) CLU(4)
+#undef CLU
   return -1;
 }

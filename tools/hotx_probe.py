@@ -20,6 +20,7 @@ if not os.path.exists(so):
                     "-Xcompiler", "-fPIC", "-lineinfo", "-o", so, os.path.join(HERE, "hotx_probe.cu")], check=True)
 L = C.CDLL(so)
 V, U64, U32, I = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
+L.hp_cluster.argtypes = [I, I, V, V, U64, V, V, U32, V, V]
 L.hp_run.argtypes = [I, I, I, V, V, U64, V, V, U32, V, V]
 
 
@@ -88,3 +89,23 @@ for H, shapes in ((2048, (0, 1, 3)), (4096, (0, 1, 3)), (8192, (1, 3, 4)), (1228
         print(f"hot H={H} ({H*8//1024} KB, {cover:.3f} of gathers) shape {shape}: rc={rc} {timeit(fn):.1f} us ok={ok}",
               flush=True)
     del col2
+
+# cluster-shared hot copies (distributed shared memory): CL CTAs x (H / CL) slots each
+for H, CL in ((12288, 1), (24576, 2), (49152, 4), (12288, 2), (24576, 4)):
+    top = torch.topk(cnt, H).indices
+    cover = float(cnt[top].sum()) / nnz
+    slot = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    slot[top] = torch.arange(H, device="cuda")
+    c64 = col.to(torch.int64) & 0xFFFFFFFF
+    sl = slot[c64]
+    col2 = torch.where(sl >= 0, (sl | 0x80000000) - (1 << 32), c64).to(torch.int32).contiguous()
+    del sl, c64
+    xh = x[top].contiguous()
+    fn = lambda: L.hp_cluster(CL, CONTIG, col2.data_ptr(), val.data_ptr(), passes, x.data_ptr(), xh.data_ptr(), H,  # noqa
+                              out.data_ptr(), s)
+    out.zero_()
+    rc = fn()
+    torch.cuda.synchronize()
+    ok = abs(out.item() - tref) <= 1e-9 * abs(tref)
+    print(f"cluster CL={CL} H={H} ({H*8//1024//CL} KB/CTA, {cover:.3f} of gathers): rc={rc} {timeit(fn):.1f} us ok={ok}",
+          flush=True)
