@@ -97,7 +97,24 @@ def test_hot_rmat(cuda, oracle, monkeypatch, scale, ef, cap, tiles):
     assert f0.info["merge_hot_slots"] == 0
     ref = oracle.build(0, m, n, r, c, v)
     xd = torch.from_numpy(x).cuda()
+    assert_y_close(sp.run_spmv(MERGE, f0, xd, p=1).cpu().numpy(), oracle.spmv(ref, 0, x),
+                   oracle.abs_spmv(m, r, c, v, x), what="without the plan")
     np.testing.assert_array_equal(sp.run_spmv(0, f, xd, p=1).cpu().numpy(), oracle.spmv(ref, 0, x))
+
+
+def test_hot_rectangular(cuda, oracle, monkeypatch):
+    """A rectangular matrix (m = 3n, then m = n / 4) with skewed columns: the plan and y."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    _, n, r, c, v = gen.rmat_host(14, 16, seed=41)
+    for m in (3 * n, n // 4):
+        rr = (r.astype(np.int64) * 2654435761 % m).astype(np.uint32)  # rows spread over m
+        key = np.unique(rr.astype(np.int64) * n + c)
+        r2, c2 = (key // n).astype(np.uint32), (key % n).astype(np.uint32)
+        v2 = np.random.default_rng(m).uniform(-1, 1, len(key))
+        f = _build(sp, monkeypatch, m, n, r2, c2, v2, SPMVLAB_MERGE_HOT_TILES=2)
+        x = np.random.default_rng(1).uniform(-1, 1, n)
+        _check(sp, oracle, f, m, n, r2, c2, v2, x, what=f"m={m} n={n}")
 
 
 def test_hot_long_and_empty_rows(cuda, oracle, monkeypatch):
