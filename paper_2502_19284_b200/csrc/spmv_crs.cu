@@ -18,9 +18,13 @@
 //    128-entry shared map, each lane walks its 4 products, one warp segmented scan joins the
 //    lanes.  Kernel and fix-up are launched with programmatic stream serialization (the next grid
 //    is resident while the previous drains; griddepcontrol.wait before any memory access).
+//    With a hot-x plan (a column-skewed matrix, build_hot_columns) the tile kernel is instead the
+//    persistent merge_hot_kernel: one 1,024-thread CTA per SM keeps x at the most referenced
+//    columns in shared memory and walks 8-wide, software-pipelined passes of 256 elements.
 //    Superseded designs and what they measured at cfg2 are listed in DESIGN.md section 4 (shared-
 //    memory / warp-staged / shuffle-only tiles, a persistent TMA bulk-copy ring, TMA gather4 x
-//    fetches); the floor for an LSU-gather kernel on R-MAT s22 is the x-gather rate.
+//    fetches, a distributed-shared-memory hot copy); the floor for an LSU-gather kernel is the
+//    L1TEX wavefront rate of the x gathers (one per gathered line).
 #include <algorithm>
 #include <cstdlib>
 #include <map>
