@@ -268,3 +268,34 @@ def test_loop_scale_drift(cuda, oracle, monkeypatch, fused):
     np.testing.assert_allclose(got, want_x, rtol=1e-10, atol=1e-300)
     if nb is not None:
         np.testing.assert_allclose(nb.cpu().numpy()[:, 1], want[:, 1], rtol=1e-10)
+
+
+@pytest.mark.parametrize("case", ["one_column", "all_columns_hot", "hot_and_empty_columns"])
+def test_hot_edge_matrices(cuda, oracle, monkeypatch, case):
+    """Every entry in one column (a 1-slot plan); every column hot (all of x in shared memory);
+    hot columns next to never-referenced ones, with some rows empty."""
+    sp = cuda
+    rng = np.random.default_rng(17)
+    if case == "one_column":
+        m, n = 50000, 1000
+        r = np.arange(0, m, 2, dtype=np.uint32)
+        c = np.full(len(r), 777, dtype=np.uint32)
+    elif case == "all_columns_hot":
+        m, n = 20000, 4096
+        key = np.unique(rng.integers(0, m, 400000).astype(np.int64) * n + rng.integers(0, n, 400000))
+        r, c = (key // n).astype(np.uint32), (key % n).astype(np.uint32)
+    else:
+        m, n = 30000, 60000
+        hot = rng.choice(n, 2000, replace=False)
+        rows = rng.integers(0, m // 2, 300000)  # rows >= m / 2 stay empty
+        cols = np.where(rng.random(300000) < 0.9, rng.choice(hot, 300000), rng.integers(0, n, 300000))
+        key = np.unique(rows.astype(np.int64) * n + cols)
+        r, c = (key // n).astype(np.uint32), (key % n).astype(np.uint32)
+    v = rng.uniform(-1, 1, len(r))
+    perm = rng.permutation(len(r))
+    r, c, v = r[perm], c[perm], v[perm]
+    f = _build(sp, monkeypatch, m, n, r, c, v)
+    x = rng.uniform(-1, 1, n)
+    _check(sp, oracle, f, m, n, r, c, v, x, what=case)
+    if case == "all_columns_hot":
+        assert f.info["merge_hot_slots"] == n
