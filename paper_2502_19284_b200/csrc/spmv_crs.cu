@@ -162,7 +162,9 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x, const d
   if constexpr (HOT) {
     double v;
     if ((int)c < 0) v = sx[c & 0x7FFFFFFFu];
-    else v = ld_x(x + c, pl);
+    else v = ld_xm<1>(x + c, pl);  // no L1 allocation: the L1 left beside the hot copy keeps its
+                                   // lines for gathers in flight (default allocate / plain / .cg:
+                                   // 271 / 271 / 265 vs 265 us at cfg2)
     return v;
   } else {
     return ld_x(x + c, pl);
