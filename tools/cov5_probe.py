@@ -1,3 +1,4 @@
+"""Dev tool: share of each column panel's gathers the hot-x slots would cover at cfg5 (R-MAT s26)."""
 import torch, sys
 sys.path.insert(0, "/root/repo")
 from paper_2502_19284_b200 import gen
