@@ -373,8 +373,11 @@ int build_merge_plan(Format& f, Arena& ar) {
   f.merge_hot = 0;
   f.merge_hot_share = 0.0;
   f.merge_persist = false;
+  f.merge_x_noalloc = false;
+  if (f.alg == kMerge) {  // the column skew, and on one panel the hot-x plan
+    if (int rc = build_hot_columns(f, ar, panels == 1)) return rc;
+  }
   if (panels == 1 && f.alg == kMerge) {
-    if (int rc = build_hot_columns(f, ar)) return rc;
     f.merge_persist = f.merge_hot > 0;
     if (f.merge_persist) {
       // equal merge-path shares, kHotTilesPerWarp per warp of the persistent grid
@@ -515,13 +518,11 @@ __global__ void hot_remap(const uint32_t* __restrict__ col, uint64_t nnz, const 
 }
 }  // namespace
 
-int build_hot_columns(Format& f, Arena& ar) {
+int build_hot_columns(Format& f, Arena& ar, bool adopt) {
   cudaStream_t s = ar.stream();
   f.merge_hot = 0;
-  uint32_t cap = kHotMaxSlots;
-  if (const char* e = getenv("SPMVLAB_MERGE_HOT_SLOTS")) cap = (uint32_t)std::max(0, std::min(atoi(e), (int)kHotMaxSlots));
-  if (const char* e = getenv("SPMVLAB_MERGE_HOT")) if (atoi(e) == 0) cap = 0;
-  if (cap == 0 || f.nnz == 0 || f.n == 0 || f.n > 0x7FFFFFFFu) return kOk;
+  f.merge_x_noalloc = false;
+  if (f.nnz == 0 || f.n == 0 || f.n > 0x7FFFFFFFu) return kOk;
   const uint32_t* col = f.find("col_ind")->as<uint32_t>();
   uint32_t* cnt = ar.alloc_n<uint32_t>((uint64_t)f.n + 1);
   uint32_t* hist = ar.alloc_n<uint32_t>(kRefBins);
@@ -534,16 +535,28 @@ int build_hot_columns(Format& f, Arena& ar) {
   std::vector<uint32_t> h(kRefBins);
   cudaMemcpyAsync(h.data(), hist, 4ull * kRefBins, cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("build_hot_columns");
+  const uint32_t min_cnt = (kHotMinRefs + samp - 1) / samp;  // counts are of the sample
+  auto select = [&](uint32_t cap, uint64_t& take, uint64_t& refs, uint32_t& thr) {
+    take = refs = 0;
+    thr = 0;
+    for (uint32_t c = kRefBins - 1; c >= min_cnt; --c) {
+      if (take + h[c] > cap) break;
+      take += h[c];
+      refs += (uint64_t)c * h[c] * samp;
+      if (h[c]) thr = c;
+    }
+    return thr != 0 && take != 0 && (double)refs >= kHotMinShare * (double)f.nnz;
+  };
   uint64_t take = 0, refs = 0;
   uint32_t thr = 0;
-  const uint32_t min_cnt = (kHotMinRefs + samp - 1) / samp;  // counts are of the sample
-  for (uint32_t c = kRefBins - 1; c >= min_cnt; --c) {
-    if (take + h[c] > cap) break;
-    take += h[c];
-    refs += (uint64_t)c * h[c] * samp;
-    if (h[c]) thr = c;
-  }
-  if (thr == 0 || take == 0 || (double)refs < kHotMinShare * (double)f.nnz) return check_launch("build_hot_columns");
+  // No column skew (the most referenced kHotMaxSlots columns cover under kHotMinShare of the
+  // entries): the merge kernels gather x without L1 allocation (cfg3 / cfg4: -3 / -2 %; on R-MAT the
+  // L1 holds the hot columns: without allocation cfg2 292 -> 389 us, cfg5 +1 %).
+  f.merge_x_noalloc = !select(kHotMaxSlots, take, refs, thr);
+  uint32_t cap = adopt ? kHotMaxSlots : 0;
+  if (const char* e = getenv("SPMVLAB_MERGE_HOT_SLOTS")) cap = (uint32_t)std::max(0, std::min(atoi(e), (int)kHotMaxSlots));
+  if (const char* e = getenv("SPMVLAB_MERGE_HOT")) if (atoi(e) == 0) cap = 0;
+  if (!adopt || cap == 0 || !select(cap, take, refs, thr)) return check_launch("build_hot_columns");
   uint32_t* flag = ar.alloc_n<uint32_t>((uint64_t)f.n + 1);
   uint32_t* colmap = ar.alloc_n<uint32_t>((uint64_t)f.n);
   uint32_t* hc = static_cast<uint32_t*>(f.add("merge_hot_col", f.nnz, 4, s));

@@ -53,6 +53,7 @@ struct spmvlab_cuda_format {
   // indices in the plan copy "merge_hot_col" carry 0x80000000 | slot, "merge_hot_cols" lists them
   uint32_t merge_hot = 0;
   bool merge_persist = false;    // persistent 8-wide tile kernel (always with a hot-x plan)
+  bool merge_x_noalloc = false;  // no column skew: the tile kernels gather x without L1 allocation
   double merge_hot_share = 0.0;  // share of the nonzeros whose x comes from the copy
 
   // ---- ParCRS launch shape

@@ -37,7 +37,8 @@ constexpr uint32_t kHotMinRefs = 32;
 constexpr double kHotMinShare = 0.10;
 constexpr uint32_t kHotTilesPerWarp = 4;
 constexpr int kHotWarps = 32;  // warps of the persistent hot-x CTA (one per SM)
-int build_hot_columns(Format& f, Arena& ar);
+// (adopt: build the plan; always: the column-skew flag merge_x_noalloc)
+int build_hot_columns(Format& f, Arena& ar, bool adopt);
 
 // ---- conversions (COO -> format); each returns a Status
 int build_crs(Format& f, const spmvlab_cuda_coo& a, Arena& ar);

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) par_crs_kernel(const uint32_t* __restrict
 // outside [j0, j1) are masked (the tile's merge-path element range is not 4-aligned).
 // x[c], or its shared-memory copy: with a hot-x plan the column index of the most referenced
 // columns carries 0x80000000 | slot (merge_hot_col) and sx holds x at those columns.
-template <bool HOT>
+template <bool HOT, bool NA = false>
 __device__ __forceinline__ double gather_x(const double* __restrict__ x, const double* sx, uint32_t c, uint64_t pl) {
   if constexpr (HOT) {
     double v;
@@ -166,12 +166,12 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x, const d
                                    // lines for gathers in flight (default allocate / plain / .cg:
                                    // 271 / 271 / 265 vs 265 us at cfg2)
     return v;
-  } else {
-    return ld_x(x + c, pl);
+  } else {  // (NA: no column skew, the L1 keeps no x worth reusing -- merge_x_noalloc)
+    return NA ? ld_xm<1>(x + c, pl) : ld_x(x + c, pl);
   }
 }
 
-template <bool HOT>
+template <bool HOT, bool NA>
 __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, const double* __restrict__ val,
                                              const double* __restrict__ x, const double* sx, uint32_t k, uint32_t j0,
                                              uint32_t j1, uint64_t pf, uint64_t pl, double p[4]) {
@@ -180,15 +180,15 @@ __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, c
     double v0, v1, v2, v3;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                  : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
-    p[0] = v0 * gather_x<HOT>(x, sx, c.x, pl);
-    p[1] = v1 * gather_x<HOT>(x, sx, c.y, pl);
-    p[2] = v2 * gather_x<HOT>(x, sx, c.z, pl);
-    p[3] = v3 * gather_x<HOT>(x, sx, c.w, pl);
+    p[0] = v0 * gather_x<HOT, NA>(x, sx, c.x, pl);
+    p[1] = v1 * gather_x<HOT, NA>(x, sx, c.y, pl);
+    p[2] = v2 * gather_x<HOT, NA>(x, sx, c.z, pl);
+    p[3] = v3 * gather_x<HOT, NA>(x, sx, c.w, pl);
   } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t e = k + u;
-      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * gather_x<HOT>(x, sx, ld_stream(col + e, pf), pl) : 0.0;
+      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * gather_x<HOT, NA>(x, sx, ld_stream(col + e, pf), pl) : 0.0;
     }
   }
 }
@@ -357,7 +357,7 @@ __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uin
 constexpr int kMergeNP = 2;
 
 // One warp tile t: the merge path's items [tile_row/nnz[t], tile_row/nnz[t + 1]).
-template <bool HOT, bool SCATTER, bool ACC, bool LAST>
+template <bool HOT, bool SCATTER, bool ACC, bool LAST, bool NA>
 __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
                                            const uint32_t* __restrict__ col, const double* __restrict__ val,
                                            const double* __restrict__ x, const double* sx, double* __restrict__ y,
@@ -379,7 +379,7 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ row_ptr,
     double p[kMergeNP][4];
 #pragma unroll
     for (int i = 0; i < kMergeNP; ++i)
-      vec_products<HOT>(col, val, x, sx, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+      vec_products<HOT, NA>(col, val, x, sx, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
 #pragma unroll
     for (int i = 0; i < kMergeNP; ++i) {
       if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
@@ -579,7 +579,7 @@ __device__ __forceinline__ void merge_tile8(const uint32_t* __restrict__ row_ptr
   __syncwarp();
 }
 
-template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST>
+template <int IPT, int WARPS, bool SCATTER, bool ACC, bool LAST, bool NA>
 __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) merge_spmv_vec_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ col,
     const double* __restrict__ val,
@@ -594,8 +594,8 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (t >= tiles) return;
-  merge_tile<false, SCATTER, ACC, LAST>(row_ptr, rows, col, val, x, nullptr, y, tile_row, tile_nnz, carry_row,
-                                        carry_val, t, s_map_all[warp], lane, dest);
+  merge_tile<false, SCATTER, ACC, LAST, NA>(row_ptr, rows, col, val, x, nullptr, y, tile_row, tile_nnz, carry_row,
+                                            carry_val, t, s_map_all[warp], lane, dest);
 }
 
 // Hot-x variant (R-MAT-like column skew; plan built by build_hot_columns): one persistent CTA of
@@ -794,8 +794,14 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
   const double* val = f.find(pan ? "merge_panel_data" : "data")->as<double>();
   const uint32_t* trow = f.find("merge_tile_row")->as<uint32_t>() + o;
   const uint32_t* tnnz = f.find("merge_tile_nnz")->as<uint32_t>() + o;
-  launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST>, (tiles + WARPS - 1) / WARPS, kMergeThreads, s,
-             rp, rows, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles, dest);
+  if (f.merge_x_noalloc)
+    launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST, true>, (tiles + WARPS - 1) / WARPS,
+               kMergeThreads, s, rp, rows, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles,
+               dest);
+  else
+    launch_pdl(merge_spmv_vec_kernel<IPT, WARPS, SCATTER, ACC, LAST, false>, (tiles + WARPS - 1) / WARPS,
+               kMergeThreads, s, rp, rows, col, val, x, y, trow, tnnz, sc->carry_row + t0, sc->carry_val + t0, tiles,
+               dest);
   launch_pdl(merge_fixup_kernel<SCATTER, LAST>, (tiles + 255) / 256, 256, s, sc->carry_row + t0,
              (const double*)(sc->carry_val + t0), tiles, y, f.panel_nrows[k], rows, dest);
 }
