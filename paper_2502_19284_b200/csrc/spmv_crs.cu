@@ -171,24 +171,25 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x, const d
   }
 }
 
-template <bool HOT, bool NA>
+template <bool NA>
 __device__ __forceinline__ void vec_products(const uint32_t* __restrict__ col, const double* __restrict__ val,
-                                             const double* __restrict__ x, const double* sx, uint32_t k, uint32_t j0,
-                                             uint32_t j1, uint64_t pf, uint64_t pl, double p[4]) {
+                                             const double* __restrict__ x, uint32_t k, uint32_t j0, uint32_t j1,
+                                             uint64_t pf, uint64_t pl, double p[4]) {
   if (k >= j0 && k + 3 < j1) {
     const uint4 c = ld_stream4(col + k, pf);
     double v0, v1, v2, v3;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                  : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(val + k), "l"(pf));
-    p[0] = v0 * gather_x<HOT, NA>(x, sx, c.x, pl);
-    p[1] = v1 * gather_x<HOT, NA>(x, sx, c.y, pl);
-    p[2] = v2 * gather_x<HOT, NA>(x, sx, c.z, pl);
-    p[3] = v3 * gather_x<HOT, NA>(x, sx, c.w, pl);
+    p[0] = v0 * gather_x<false, NA>(x, nullptr, c.x, pl);
+    p[1] = v1 * gather_x<false, NA>(x, nullptr, c.y, pl);
+    p[2] = v2 * gather_x<false, NA>(x, nullptr, c.z, pl);
+    p[3] = v3 * gather_x<false, NA>(x, nullptr, c.w, pl);
   } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t e = k + u;
-      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * gather_x<HOT, NA>(x, sx, ld_stream(col + e, pf), pl) : 0.0;
+      p[u] = (e >= j0 && e < j1) ? ld_stream(val + e, pf) * gather_x<false, NA>(x, nullptr, ld_stream(col + e, pf), pl)
+                                   : 0.0;
     }
   }
 }
@@ -239,37 +240,6 @@ __device__ __forceinline__ void row_ends(const uint32_t* __restrict__ row_ptr, c
     if (nin) prevE = __shfl_sync(0xFFFFFFFFu, E, nin - 1);
     rp += (uint32_t)nin;
     if (nin < 32) break;
-  }
-}
-
-// The same from a row window prefetched at the start of the pass group: wE = row_ptr[wb + 1 + lane]
-// for rows wb + lane < r1 (wS0 = row_ptr[wb]); rows before rp are already closed.  The window moves
-// (a dependent reload) only when all its 32 rows close within the group.
-template <bool SCATTER, bool ACC, bool LAST>
-__device__ __forceinline__ void row_ends_win(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
-                                             double* __restrict__ y, uint32_t* smap, uint32_t base, uint32_t pend,
-                                             uint32_t j0, uint32_t r1, uint32_t& rp, uint32_t& prevE, uint32_t& wb,
-                                             uint32_t& wE, uint32_t& wS0, unsigned lane, const RowDest& dest) {
-  while (rp < r1) {
-    const uint32_t idx = wb + lane;
-    uint32_t S = __shfl_up_sync(0xFFFFFFFFu, wE, 1);
-    if (lane == 0) S = wS0;
-    const bool in = idx >= rp && idx < r1 && wE <= pend;
-    if (in) {
-      if (wE == S || wE <= j0) {
-        if (!ACC) put_row_m<SCATTER, ACC, LAST>(y, rows, dest, idx, 0.0);
-      }
-      else smap[wE - 1 - base] = idx + 1u;
-    }
-    const unsigned inmask = __ballot_sync(0xFFFFFFFFu, in);
-    if (inmask) {
-      prevE = __shfl_sync(0xFFFFFFFFu, wE, 31 - __clz(inmask));
-      rp += (uint32_t)__popc(inmask);
-    }
-    if (rp < wb + 32u || rp >= r1) break;
-    wb = rp;  // every row of the window closed: the next 32
-    wS0 = prevE;
-    wE = wb + lane < r1 ? __ldg(row_ptr + wb + 1 + lane) : 0xFFFFFFFFu;
   }
 }
 
@@ -357,10 +327,10 @@ __device__ __forceinline__ void push_rows(const double* y, const RowDest& d, uin
 constexpr int kMergeNP = 2;
 
 // One warp tile t: the merge path's items [tile_row/nnz[t], tile_row/nnz[t + 1]).
-template <bool HOT, bool SCATTER, bool ACC, bool LAST, bool NA>
+template <bool SCATTER, bool ACC, bool LAST, bool NA>
 __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows,
                                            const uint32_t* __restrict__ col, const double* __restrict__ val,
-                                           const double* __restrict__ x, const double* sx, double* __restrict__ y,
+                                           const double* __restrict__ x, double* __restrict__ y,
                                            const uint32_t* __restrict__ tile_row,
                                            const uint32_t* __restrict__ tile_nnz, uint32_t* __restrict__ carry_row,
                                            double* __restrict__ carry_val, uint32_t t, uint32_t* smap,
@@ -379,7 +349,7 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ row_ptr,
     double p[kMergeNP][4];
 #pragma unroll
     for (int i = 0; i < kMergeNP; ++i)
-      vec_products<HOT, NA>(col, val, x, sx, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
+      vec_products<NA>(col, val, x, base + 128u * i + 4 * lane, j0, j1, pf, pl, p[i]);
 #pragma unroll
     for (int i = 0; i < kMergeNP; ++i) {
       if (i > 0 && !(base + 128u * i < j1 || rp < r1)) {
@@ -594,8 +564,8 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (t >= tiles) return;
-  merge_tile<false, SCATTER, ACC, LAST, NA>(row_ptr, rows, col, val, x, nullptr, y, tile_row, tile_nnz, carry_row,
-                                            carry_val, t, s_map_all[warp], lane, dest);
+  merge_tile<SCATTER, ACC, LAST, NA>(row_ptr, rows, col, val, x, y, tile_row, tile_nnz, carry_row, carry_val, t,
+                                     s_map_all[warp], lane, dest);
 }
 
 // Hot-x variant (R-MAT-like column skew; plan built by build_hot_columns): one persistent CTA of
