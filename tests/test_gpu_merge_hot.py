@@ -299,3 +299,27 @@ def test_hot_edge_matrices(cuda, oracle, monkeypatch, case):
     _check(sp, oracle, f, m, n, r, c, v, x, what=case)
     if case == "all_columns_hot":
         assert f.info["merge_hot_slots"] == n
+
+
+def test_hot_concurrent_streams(cuda, oracle, monkeypatch):
+    """One hot-x format multiplied on four streams at once (per-stream carry scratch; the persistent
+    grids of different streams share the SMs)."""
+    from paper_2502_19284_b200 import gen
+    sp = cuda
+    m, n, r, c, v = gen.rmat_host(14, 16, seed=55)
+    f = _build(sp, monkeypatch, m, n, r, c, v)
+    assert f.info["merge_hot_slots"] > 0
+    ref = oracle.build(0, m, n, r, c, v)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    xs = [np.random.default_rng(200 + i).uniform(-1, 1, n) for i in range(4)]
+    xd = [torch.from_numpy(x).cuda() for x in xs]
+    ys = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in range(4)]
+    torch.cuda.synchronize()
+    for _ in range(5):
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                sp.run_spmv(MERGE, f, xd[i], ys[i], p=1, stream=s)
+    torch.cuda.synchronize()
+    for i in range(4):
+        assert_y_close(ys[i].cpu().numpy(), oracle.spmv(ref, 0, xs[i]), oracle.abs_spmv(m, r, c, v, xs[i]),
+                       what=f"stream {i}")
