@@ -737,17 +737,6 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned threads
 // Panel k of a column-panelled format (k = 0 and one panel: the plain CRS arrays), then its carry
 // fix-up.  The fix-up of panel k runs before panel k + 1's kernel (stream order; PDL waits for full
 // completion), so the accumulating panels read final sums.
-// Copies rows [0, m) of y to every peer (the fused exchange of a column-panelled multiply: its
-// rows are final only after the last panel's fix-up).
-__global__ void push_all_rows(const double* __restrict__ y, uint32_t m, const __grid_constant__ RowDest dest) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += stride) {
-    const double v = y[r];
-    for (unsigned i = 0; i < dest.n; ++i) dest.p[i][dest.off + r] = v;
-  }
-}
-
 template <int IPT, bool SCATTER, bool ACC, bool LAST>
 void launch_merge_panel(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
                         const RowDest& dest, uint32_t k) {
@@ -776,8 +765,8 @@ void launch_merge_panel(const Format& f, const double* x, double* y, const Scrat
              (const double*)(sc->carry_val + t0), tiles, y, f.panel_nrows[k], rows, dest);
 }
 
-// The tile kernels' own peer push (SCATTER) is used without panels; a panelled multiply pushes
-// all its rows after the last panel (push_all_rows).
+// The tile kernels' own peer push (SCATTER): the single panel, or panel 0 of a panelled multiply
+// run last (launch_merge_panels_scatter).
 // The persistent plan (one panel only; with or without hot x): merge_hot_kernel, then the carry fix-up.
 template <bool HOT, bool SCATTER>
 void launch_merge_persistent(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
@@ -812,6 +801,25 @@ void launch_merge_persistent(const Format& f, const double* x, double* y, const 
              (const double*)sc->carry_val, tiles, y, f.m, (const uint32_t*)nullptr, dest);
 }
 
+// A column-panelled multiply with row destinations (the fused multi-GPU exchange): y is cleared,
+// the panels k >= 1 accumulate first, and panel 0 -- the one walking every row, on R-MAT the bulk
+// of the entries -- runs LAST, accumulating, with each warp tile copying the rows it finished to the
+// peers as it ends (rows with no entries in panel 0 are already final, and so pushed too; the carry
+// fix-up pushes the rest), so the exchange overlaps the largest panel's compute instead of following
+// all of it.  The panel sums are added in the order 1, ..., K-1, 0 here (0, 1, ..., K-1 without
+// destinations): the two results agree within the summation tolerance, not bitwise.
+template <int IPT>
+void launch_merge_panels_scatter(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
+                                 const RowDest& dest) {
+  cudaMemsetAsync(y, 0, sizeof(double) * f.m, s);
+  for (uint32_t k = 1; k < f.merge_panels; ++k) {
+    launch_merge_panel<IPT, false, true, false>(f, x, y, sc, s, dest, k);
+    if (f.panel_tile_off[k + 1] > f.panel_tile_off[k]) note_launch(2);
+  }
+  launch_merge_panel<IPT, true, true, true>(f, x, y, sc, s, dest, 0);
+  if (f.panel_tile_off[1] > f.panel_tile_off[0]) note_launch(2);
+}
+
 template <int IPT>
 void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch* sc, cudaStream_t s,
                       const RowDest& dest, uint32_t k) {
@@ -825,10 +833,6 @@ void launch_merge_ipt(const Format& f, const double* x, double* y, const Scratch
     launch_merge_panel<IPT, false, true, false>(f, x, y, sc, s, dest, k);
   } else {
     launch_merge_panel<IPT, false, true, true>(f, x, y, sc, s, dest, k);
-    if (dest.n) {
-      launch_pdl(push_all_rows, grid_for(f.m, 256), 256, s, (const double*)y, f.m, dest);
-      note_launch();
-    }
   }
 }
 
@@ -945,6 +949,15 @@ int spmv_merge(const Format& f, const double* x, double* y, cudaStream_t s, cons
     return check_launch("spmv_merge");
   }
   timing_begin("merge_spmv_vec_kernel", s);
+  if (dest.n && f.merge_panels > 1) {
+    switch (f.merge_ipt) {
+      case 8: launch_merge_panels_scatter<8>(f, x, y, sc, s, dest); break;
+      case 16: launch_merge_panels_scatter<16>(f, x, y, sc, s, dest); break;
+      default: launch_merge_panels_scatter<32>(f, x, y, sc, s, dest); break;
+    }
+    timing_end(s);
+    return check_launch("spmv_merge");
+  }
   for (uint32_t k = 0; k < f.merge_panels; ++k) {
     switch (f.merge_ipt) {
       case 8: launch_merge_ipt<8>(f, x, y, sc, s, dest, k); break;

@@ -115,8 +115,13 @@ def test_scatter_single_rank_equals_run_spmv(cuda, monkeypatch, panels):
     _check(capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, x.data_ptr(), n, y.data_ptr(), m, dest, 1, m + 5,
                                                      5, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    assert torch.equal(y, y_ref)
-    assert torch.equal(d1[5:], y_ref) and bool((d1[:5] == -1.0).all())
+    if panels:  # panel 0 runs last with destinations: the same sums in another order
+        from parity import assert_y_close
+        bound = sp.run_spmv(2, sp.build_format(2, sp.TripletMatrix.from_host(m, n, r, c, np.abs(v)), 1), x.abs())
+        assert_y_close(y.cpu().numpy(), y_ref.cpu().numpy(), bound.cpu().numpy(), what=f"panels={panels}")
+    else:
+        assert torch.equal(y, y_ref)
+    assert torch.equal(d1[5:], y) and bool((d1[:5] == -1.0).all())
     # a destination too short for row_offset + m is rejected before anything is written
     rc = capi.load().spmvlab_cuda_run_spmv_scatter(f.handle, x.data_ptr(), n, y.data_ptr(), m, dest, 1, m + 4, 5,
                                                    torch.cuda.current_stream().cuda_stream)
