@@ -29,9 +29,10 @@ constexpr int kAutoMergePanels = 3;
 constexpr uint64_t kPanelXBytes = 96ull << 20;
 bool merge_shape_supported(int threads, int ipt);
 // Hot-x plan of the merge engine (build_hot_columns, convert_crs.cu): at most kHotMaxSlots x
-// entries (96 KB of shared memory per SM, with 16 KB of row maps) for the columns referenced at least kHotMinRefs times,
-// kept when they cover at least kHotMinShare of the nonzeros; the persistent tile kernel then runs
-// kHotTilesPerWarp tiles per resident warp (equal merge-path shares).
+// entries (96 KB of shared memory per SM, beside 16 KB of row maps: more shared memory starves the
+// L1 the gathers need in flight) for the columns referenced at least kHotMinRefs times (sampled
+// counts), kept when they cover at least kHotMinShare of the nonzeros; the persistent tile kernel
+// then runs kHotTilesPerWarp tiles per resident warp (equal merge-path shares).
 constexpr uint32_t kHotMaxSlots = 12288;
 constexpr uint32_t kHotMinRefs = 32;
 constexpr double kHotMinShare = 0.10;

@@ -572,7 +572,9 @@ __global__ void __launch_bounds__(WARPS * 32, (kMergeNP > 2 ? 40 : 48) / WARPS) 
 // kHotWarps warps per SM.  The CTA first copies x at the plan's hot columns (merge_hot_cols, the
 // most referenced ones) into shared memory; its warps then walk tiles t = warp id, + grid warps,
 // ... with those columns read from shared memory (LDS: a few bank wavefronts per warp instead of
-// one L2 sector per lane) and the rest gathered from the L2 as usual.
+// one L2 sector per lane) and the rest gathered from the L2 without L1 allocation (the L1 left
+// beside the hot copy holds the gathers in flight).  NORMS (the rescaled loop without norms): the
+// products are scaled by the loop's drift factor and summed per CTA for the mass.
 template <bool HOT, bool SCATTER, bool NORMS = false>
 __global__ void __launch_bounds__(kHotWarps * 32, 1) merge_hot_kernel(
     const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, const double* __restrict__ val,
